@@ -1,0 +1,269 @@
+/*
+ * adacluster_sm100.h — C-ABI of the B200-native AdaCluster hot path.
+ *
+ * This is the drop-in boundary for the cluster -> select -> sparse-attention
+ * path of the reference package `adacluster` 0.1.0 (pure Python/numpy, see
+ * /root/reference/pkg/src/adacluster).  The reference has no FFI of its own;
+ * its public Python surface (`__init__.py:3-41`) is re-implemented by
+ * `paper_2604_18348_b200/` on top of these entry points, loaded with ctypes
+ * (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - every entry point returns an int status (AC_OK ... AC_ERR_CUDA); the
+ *     message of the last failure on the calling thread is ac_last_error().
+ *     Status codes map to the reference exception classes (errors.py:8-29):
+ *     AC_ERR_PARAM -> ParameterError, AC_ERR_DIM -> DimensionError,
+ *     AC_ERR_CONTRACT -> ContractError.
+ *   - all pointers are DEVICE pointers owned by the caller unless a comment
+ *     says "host"; the library never allocates or frees caller memory.
+ *   - all work is enqueued on the caller's cudaStream_t (passed as void*);
+ *     no entry point synchronises unless documented.
+ *   - matrices are row-major, rows contiguous.  dtype is AC_DTYPE_F32 or
+ *     AC_DTYPE_BF16 for token tensors; centres/envelopes/scores are f32.
+ */
+#ifndef ADACLUSTER_SM100_H
+#define ADACLUSTER_SM100_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AC_ABI_VERSION 1
+
+/* status codes */
+#define AC_OK 0
+#define AC_ERR_PARAM 1
+#define AC_ERR_DIM 2
+#define AC_ERR_CONTRACT 3
+#define AC_ERR_CUDA 4
+
+/* token tensor element types */
+#define AC_DTYPE_F32 0
+#define AC_DTYPE_BF16 1
+
+/* Accumulation order of an f32 NT product x @ c.T with inner length D.
+ * The reference's `@` is OpenBLAS sgemm; its order depends on the shape
+ * and is reproduced exactly:
+ *   AC_ORDER_SEQ     acc = fmaf(x[t], c[t], acc), t = 0..D-1, from 0
+ *   AC_ORDER_LANES16 16 lane chains (t mod 16) + adjacent-pair tree
+ *   AC_ORDER_GEMV8   8 lane chains (t mod 8), s[l]=a[l]+a[l+4], (s0+s1)+(s2+s3)
+ * ac_gemm_order() returns the order the reference uses for an M x N x D call. */
+#define AC_ORDER_SEQ 0
+#define AC_ORDER_LANES16 1
+#define AC_ORDER_GEMV8 2
+
+/* TensorQuest scorer variants (pipeline.py:144-151) */
+#define AC_SCORER_QUEST 0   /* quest.py:94   max(Q,0)·maxᵀ + min(Q,0)·minᵀ     */
+#define AC_SCORER_MEAN 1    /* quest.py:119  Q·centersᵀ                        */
+#define AC_SCORER_CLAMPED 2 /* quest.py:106  max(Q,0)·max(C,0)ᵀ + min(Q,0)·min(C,0)ᵀ */
+
+/* ac_assign flags */
+#define AC_ASSIGN_MERGE 1   /* merge into existing (labels,best) with strict '<'
+                               so earlier (lower-index) centres win ties        */
+#define AC_ASSIGN_ALL 2     /* ignore the per-problem 'active' flag            */
+
+/* ---------------------------------------------------------------------------
+ * One clustering problem (one head, or one multi-stage round of one head).
+ * The caller allocates every buffer; sizes in brackets.  A batch of problems
+ * is an array of these in DEVICE memory; all share dtype and D.
+ * ------------------------------------------------------------------------- */
+typedef struct ac_cluster_problem {
+  const void* x;        /* [n, d] points (dtype of the batch)                 */
+  float* xx;            /* [n]   pairwise ||x_i||^2  (written by ac_lloyd_prepare) */
+  float* centers;       /* [kcap, d] in: initial centres, out: final centres  */
+  float* cc;            /* [kcap]  ||c||^2 of the current centres             */
+  int32_t* labels;      /* [n]   assignment                                   */
+  float* best;          /* [n]   assigned squared distance / k-means++ closest */
+  int32_t* counts;      /* [kcap] members per centre                          */
+  int32_t* perm;        /* [n]   stable argsort of labels (member order)      */
+  int32_t* starts;      /* [kcap+1] segment starts into perm                  */
+  int32_t* tile_hist;   /* [ceil(n/128) * kcap] per-tile label histogram      */
+  float* inertia;       /* [max_iter] inertia_history                         */
+  float* movement;      /* [kcap] per-centre movement scratch                 */
+  int32_t* status;      /* [8] {active, n_iter, done, flags, kpp_stop, ...}   */
+  const int32_t* plan_n;/* pairwise-sum plan of length n (ac_pw_plan_build)   */
+  const int32_t* plan_k;/* pairwise-sum plan of length k                      */
+  double* dscratch;     /* [n] f64 scratch (k-means++ cdf, tau)               */
+  int64_t n;
+  int32_t k;
+  int32_t order;        /* AC_ORDER_* of the reference's x @ centres.T        */
+} ac_cluster_problem;
+
+/* status[] slots */
+#define AC_ST_ACTIVE 0
+#define AC_ST_NITER 1
+#define AC_ST_DONE 2
+#define AC_ST_FLAGS 3
+#define AC_ST_KPP_STOP 4
+#define AC_ST_REPAIRS 5
+
+/* ---- library ---------------------------------------------------------- */
+const char* ac_last_error(void);
+int ac_abi_version(void);
+/* Number of SMs / compute capability of the current device (host query). */
+int ac_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- host helpers ----------------------------------------------------- */
+/* numpy pairwise-summation tree for a length-n reduction, flattened into an
+ * int32 program (ac_pw_plan_len words) executed by the reduction kernels.   */
+int64_t ac_pw_plan_len(int64_t n);
+int ac_pw_plan_build(int64_t n, int32_t* host_out, int64_t cap);
+/* OpenBLAS dispatch of the reference's f32 `a @ b.T` ([m,d] x [n,d]) */
+int ac_gemm_order(int64_t m, int64_t n, int64_t d);
+
+/* ---- K1 tensorops.py:59-76 l2_normalize_rows ---------------------------
+ * out[i] = x[i] / ||x[i]||  (numpy pairwise-8 norm, f32 divide), rows with
+ * |norm-1| <= 2e-6 copied unchanged, norm < 1e-12 -> zeros + degenerate[i]=1.
+ * Also emits xx[i] = pairwise ||out[i]||^2 for the assignment kernel.      */
+int ac_l2norm(const void* x, int dtype, int64_t rows, int d, float* out,
+              float* out_sqnorm, uint8_t* degenerate, void* stream);
+
+/* pairwise ||x_i||^2 in f32 (clustering.py:71 `(x * x).sum(axis=1)`) */
+int ac_row_sqnorm(const void* x, int dtype, int64_t rows, int d, float* out,
+                  void* stream);
+
+/* ---- K2 clustering.py:78-91 _kmeanspp_init ------------------------------
+ * draws: [nprob * max_k] f64 per problem (host-drawn numpy PCG64 stream):
+ *   draws[0] = first index (rng.integers(n)),
+ *   draws[i] = u_i = rng.random() for step i >= 1, or -(idx+1) to force the
+ *              `total <= 0` branch's rng.integers(n) result.
+ * On `total <= 0` at a step whose draw is not forced, status[AC_ST_KPP_STOP]
+ * receives the step and the problem stops (the host redraws and relaunches). */
+int ac_kmeanspp(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                int64_t max_n, int max_k, const double* draws, void* stream);
+
+/* ---- K3..K6 clustering.py:119-152 _lloyd ---------------------------------
+ * Runs up to max_iter Lloyd iterations (assign, empty repair, inertia,
+ * stable segment sort, f64 centroid update, movement < tol) for every problem
+ * and the final assign + repair + member sort.  Per-problem convergence is
+ * tracked on device (status[]); no host synchronisation unless
+ * poll_every > 0 (then the host polls every poll_every iterations and stops
+ * launching once every problem has converged).                            */
+int ac_lloyd(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+             int64_t max_n, int max_k, int max_iter, double tol,
+             int poll_every, const ac_cluster_problem* host_probs, void* stream);
+
+/* Single passes, exposed for the multi-stage planner and for tests. */
+int ac_lloyd_prepare(const ac_cluster_problem* probs, int nprob, int dtype,
+                     int d, int64_t max_n, int max_k, void* stream);
+int ac_assign(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+              int64_t max_n, int max_k, int c_lo, int flags, void* stream);
+/* same with an explicit accumulation order (AC_ORDER_*) for the batch      */
+int ac_assign_ordered(const ac_cluster_problem* probs, int nprob, int dtype,
+                      int d, int64_t max_n, int max_k, int c_lo, int flags,
+                      int order, void* stream);
+int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dtype,
+                   int d, int64_t max_n, int max_k, int iter, int flags,
+                   void* stream);
+/* segment means in f64 over members (clustering.py:134-139, :197-200):
+ * out[c] = f32(sum_{i in seg c, member order} f64(x[perm[i]]) / count[c]) */
+int ac_segment_mean(const ac_cluster_problem* probs, int nprob, int dtype,
+                    int d, int max_k, float* const* out, void* stream);
+
+/* ---- multi-stage helpers (clustering.py:209-320) ----------------------- */
+/* f32 sum over n of best[] in numpy pairwise order -> out[p] (f32) and the
+ * f32 mean f32(f64(sum)/n) -> mean_out[p] (either may be NULL)             */
+int ac_reduce_best(const ac_cluster_problem* probs, int nprob, int64_t max_n,
+                   float* sum_out, float* mean_out, void* stream);
+/* compute_tau: tau = factor * mean_n ||f64(x) - f64(c[label])|| (f64)     */
+int ac_tau(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+           int64_t max_n, double factor, double* tau_out, void* stream);
+/* per-layer MSE (pipeline.py:319-323): mean_n sum_d (f64 x - f64 c)^2    */
+int ac_mse_f64(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+               int64_t max_n, double* out, void* stream);
+/* retire distances ||x - c[label]|| (f32 pairwise-8 + sqrtf) and the
+ * order-preserving compaction U' = U[dist >= tau32]:
+ *   idx_in [n] (original row ids), idx_out [n], out_count[p] (device)     */
+int ac_retire(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+              int64_t max_n, const float* tau32, const int64_t* const* idx_in,
+              int64_t* const* idx_out, int64_t* out_count, void* stream);
+/* gather rows: dst[i] = src[idx[i]] (row = d elements of dtype)            */
+int ac_gather_rows(const void* src, int dtype, int d, const int64_t* idx,
+                   int64_t rows, void* dst, void* stream);
+/* drop centres without members and remap labels (clustering.py:303-310).
+ * counts must hold the bincount of labels; new_k[p] receives |keep|.       */
+int ac_drop_empty(const ac_cluster_problem* probs, int nprob, int d,
+                  int64_t max_n, int max_k, int32_t* new_k, void* stream);
+
+/* ---- K9..K11 quest.py:61-143 -------------------------------------------
+ * envelopes (segmented max/min over member order) for each problem.       */
+int ac_envelopes(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                 int max_k, float* const* env_max, float* const* env_min,
+                 void* stream);
+
+typedef struct ac_select_problem {
+  const float* reps;     /* [gq, d] query representatives                     */
+  const float* emax;     /* [c, d]  envelope max (or centres for MEAN/CLAMPED) */
+  const float* emin;     /* [c, d]  envelope min                              */
+  const int32_t* counts; /* [c]     key cluster sizes                         */
+  const int32_t* kstarts;/* [c+1]   key segment starts (member order)         */
+  float* scores;         /* [gq, c] out                                       */
+  int64_t* selected;     /* [gq, topk] out, descending score, ties -> low idx */
+  int32_t* runs;         /* [gq, run_stride, 2] out: merged [start,end) ranges */
+  int32_t* nruns;        /* [gq] out                                          */
+  int64_t* covered;      /* [gq] out: key tokens covered by the selection     */
+  double* density;       /* [1] out                                           */
+  int32_t gq, c, topk;   /* topk here is min(topk, c) (pipeline.py:192)      */
+  int32_t order;         /* AC_ORDER_* of the (gq x c x d) products           */
+  int32_t run_stride;    /* runs row stride (>= topk), uniform over a batch   */
+  int32_t pad_;
+} ac_select_problem;
+
+int ac_select(const ac_select_problem* probs, int nprob, int d, int scorer,
+              int max_gq, int max_c, int max_topk, void* stream);
+
+/* One attention work item = one tile of <= 128 query rows of one query
+ * cluster of one head (see ac_sparse_attention).                          */
+typedef struct ac_attn_item {
+  int64_t q_row0;        /* first row in the permuted query matrix Qp       */
+  int32_t q_rows;        /* rows in this tile (<= 128)                       */
+  int32_t head;          /* head index (selects Kp/Vp/out base)             */
+  int32_t run0;          /* first run in the runs table                     */
+  int32_t nruns;         /* number of [start,end) runs                       */
+} ac_attn_item;
+
+/* ---- K12 permutation -----------------------------------------------------
+ * dst[j] = src[perm[j]] for j < n (row gather, 16-byte vectors)            */
+int ac_permute_rows(const void* src, int dtype, int d, const int32_t* perm,
+                    int64_t n, void* dst, void* stream);
+
+/* Query layout for the attention kernel (pipeline.py:154-165): per head h,
+ * every query cluster g becomes a contiguous block of Qp rows padded to a
+ * multiple of 128, and one work item per 128-row tile is emitted.
+ *   q       [heads, L, d] queries (dtype), qperm/qstarts/qcounts/qlabels the
+ *           query clustering of each head (member order), gq clusters per head
+ *   qp      [heads * qp_cap, d] out (qp_cap = L + 128 * gq_max)
+ *   qidx    [heads * qp_cap] out: original token of each Qp row or -1
+ *   items   [heads * item_cap] out (item_cap = ceil(L/128) + gq_max); unused
+ *           slots get q_rows = 0.  Item (h, g, tile) uses runs
+ *           [(h*gq_max + g) * topk_max ...] with nruns[h*gq_max + g] runs.   */
+int ac_build_q_layout(const void* q, int dtype, int d, int64_t L, int heads,
+                      const int32_t* qperm, const int32_t* qstarts,
+                      const int32_t* qcounts, const int32_t* qlabels,
+                      const int32_t* gq, int gq_max, const int32_t* nruns,
+                      int topk_max, void* qp, int32_t* qidx, int64_t qp_cap,
+                      ac_attn_item* items, int item_cap, void* stream);
+
+/* ---- K13/K14 block-sparse attention --------------------------------------
+ * One work item = one tile of <= 128 query rows of one query cluster of one
+ * head.  Keys/values are in cluster-contiguous order (Kp/Vp, member order);
+ * the item attends over the union of [start,end) runs of Kp.               */
+
+/* q:  Qp [total_q_rows, d] (dtype), rows grouped per item
+ * qidx: [total_q_rows] original token index of each Qp row (-1 = padding)
+ * k/v: Kp/Vp [heads, L, d] (dtype), runs: [*, 2] int32 ranges into [0, L)
+ * out: [heads, L, d] f32 or bf16 (out_dtype), written at original rows.
+ * scale: softmax scale (1/sqrt(d) in the reference, reference.py:39).     */
+int ac_sparse_attention(const void* q, const int32_t* qidx, const void* k,
+                        const void* v, int dtype, int d, int64_t L,
+                        const ac_attn_item* items, int nitems,
+                        const int32_t* runs, float scale, void* out,
+                        int out_dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADACLUSTER_SM100_H */

@@ -1,0 +1,145 @@
+// C-ABI glue: error reporting, device queries, host helpers (numpy pairwise
+// plan, OpenBLAS order dispatch) and the attention dispatcher.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+namespace ac_host {
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+int check_cuda(cudaError_t e, const char* what) {
+  set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+  return AC_ERR_CUDA;
+}
+}  // namespace ac_host
+
+extern "C" const char* ac_last_error(void) { return g_last_error.c_str(); }
+extern "C" int ac_abi_version(void) { return AC_ABI_VERSION; }
+
+extern "C" int ac_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return ac_host::check_cuda(e, "cudaGetDevice");
+  cudaDeviceProp p;
+  e = cudaGetDeviceProperties(&p, dev);
+  if (e != cudaSuccess) return ac_host::check_cuda(e, "cudaGetDeviceProperties");
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  return AC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// numpy pairwise-sum plan (layout documented in pairwise.cuh)
+// ---------------------------------------------------------------------------
+namespace {
+struct PlanNode { int a, b, height; };
+struct PlanBuilder {
+  std::vector<int32_t> leaves;  // leaf start offsets (DFS order)
+  std::vector<PlanNode> internal;
+  std::vector<int> leaf_height;  // always 0
+  // returns encoded id: >= 0 leaf index, < 0 -(internal index + 1)
+  int build(int64_t lo, int64_t n, int& height) {
+    if (n <= 128) {
+      leaves.push_back((int32_t)lo);
+      height = 0;
+      return (int)leaves.size() - 1;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    int ha, hb;
+    const int a = build(lo, n2, ha);
+    const int b = build(lo + n2, n - n2, hb);
+    height = (ha > hb ? ha : hb) + 1;
+    internal.push_back({a, b, height});
+    return -(int)internal.size();
+  }
+};
+std::vector<int32_t> make_plan(int64_t n) {
+  PlanBuilder pb;
+  int h = 0;
+  pb.build(0, n, h);
+  const int L = (int)pb.leaves.size();
+  const int I = (int)pb.internal.size();
+  auto resolve = [&](int id) { return id >= 0 ? id : L + (-id - 1); };
+  int H = 0;
+  for (auto& nd : pb.internal) H = nd.height > H ? nd.height : H;
+  std::vector<int32_t> plan;
+  plan.push_back(L);
+  plan.push_back(I);
+  plan.push_back(H);
+  for (int i = 0; i < L; ++i) plan.push_back(pb.leaves[i]);
+  plan.push_back((int32_t)n);
+  // level boundaries: internal nodes grouped by height 1..H
+  std::vector<int> count(H + 2, 0);
+  for (auto& nd : pb.internal) count[nd.height]++;
+  int acc = 0;
+  for (int hh = 1; hh <= H; ++hh) { plan.push_back(acc); acc += count[hh]; }
+  plan.push_back(acc);
+  for (int hh = 1; hh <= H; ++hh)
+    for (int j = 0; j < I; ++j)
+      if (pb.internal[j].height == hh) {
+        plan.push_back(L + j);
+        plan.push_back(resolve(pb.internal[j].a));
+        plan.push_back(resolve(pb.internal[j].b));
+      }
+  return plan;
+}
+}  // namespace
+
+extern "C" int64_t ac_pw_plan_len(int64_t n) {
+  if (n < 0) return -1;
+  return (int64_t)make_plan(n).size();
+}
+
+extern "C" int ac_pw_plan_build(int64_t n, int32_t* host_out, int64_t cap) {
+  if (n < 0 || n > (int64_t)INT32_MAX) { ac_host::set_error("plan: bad n=%lld", (long long)n); return AC_ERR_PARAM; }
+  std::vector<int32_t> p = make_plan(n);
+  if ((int64_t)p.size() > cap) { ac_host::set_error("plan: capacity %lld < %zu", (long long)cap, p.size()); return AC_ERR_PARAM; }
+  std::memcpy(host_out, p.data(), p.size() * sizeof(int32_t));
+  return AC_OK;
+}
+
+// OpenBLAS 0.3.30 (SkylakeX) dispatch of the reference's f32 `a @ b.T`
+// (numpy matmul -> cblas_sgemm / gemv), measured in the oracle host
+// (re-probed by oracle/probe_blas.py).
+// Measured rules: a unit dimension goes to sgemv; M*N <= 1200 with D >= 32
+// goes to the AVX-512 small-matrix kernel (16 lane chains; elements in the
+// (M%4) x (N%4) corner reduce with the halves tree); everything else is the
+// general kernel's sequential chain.
+extern "C" int ac_gemm_order(int64_t m, int64_t n, int64_t d) {
+  if (m == 1 || n == 1) return AC_ORDER_GEMV8;
+  if (m * n <= 1200 && d >= 32) return AC_ORDER_LANES16;
+  return AC_ORDER_SEQ;
+}
+
+// ---------------------------------------------------------------------------
+// attention dispatch: tcgen05 kernel for bf16 / D in {64,128}, CUDA cores
+// otherwise (f32 inputs need f32 numerics for the 1e-4 parity bar)
+// ---------------------------------------------------------------------------
+extern "C" int ac_sparse_attention_simt(const void* q, const int32_t* qidx, const void* k,
+                                        const void* v, int dtype, int d, int64_t L,
+                                        const ac_attn_item* items, int nitems, const int32_t* runs,
+                                        float scale, void* out, int out_dtype, void* stream);
+
+extern "C" int ac_sparse_attention(const void* q, const int32_t* qidx, const void* k, const void* v,
+                                   int dtype, int d, int64_t L, const ac_attn_item* items,
+                                   int nitems, const int32_t* runs, float scale, void* out,
+                                   int out_dtype, void* stream) {
+  return ac_sparse_attention_simt(q, qidx, k, v, dtype, d, L, items, nitems, runs, scale, out,
+                                  out_dtype, stream);
+}

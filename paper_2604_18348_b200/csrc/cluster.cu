@@ -1,0 +1,1126 @@
+// Clustering kernels: row norms, l2 normalisation, k-means++ seeding,
+// the Lloyd iteration (assign -> empty repair -> inertia -> stable segment
+// sort -> f64 centroid update -> movement), and the multi-stage helpers.
+//
+// Reference: /root/reference/pkg/src/adacluster/clustering.py and
+// tensorops.py.  Every arithmetic step reproduces numpy's f32/f64 semantics
+// (pairwise sums, non-fused products, first-index argmin/argmax, f64 centre
+// sums in member order), so labels and centres are bit-identical to the
+// reference.  Compiled with --fmad=false.
+#include <cfloat>
+#include <climits>
+
+#include "common.cuh"
+#include "pairwise.cuh"
+
+namespace ac {
+
+// ---------------------------------------------------------------------------
+// numpy elementwise semantics that differ from the CUDA intrinsics on
+// signed zeros: np.maximum(a, b) = (a >= b || isnan(a)) ? a : b
+// ---------------------------------------------------------------------------
+AC_DEV float np_maximum(float a, float b) { return (a >= b || isnan(a)) ? a : b; }
+AC_DEV float np_minimum(float a, float b) { return (a <= b || isnan(a)) ? a : b; }
+
+// f32 NT dot product in the accumulation order of the reference's sgemm.
+template <typename GetX, typename GetC>
+AC_DEV float ordered_dot(const GetX& gx, const GetC& gc, int d, int order, bool halves = false) {
+  if (order == AC_ORDER_LANES16) {
+    float r[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) r[j] = 0.f;
+    for (int t = 0; t < d; ++t) r[t & 15] = __fmaf_rn(gx(t), gc(t), r[t & 15]);
+    float s[8], u[4];
+    if (halves) {  // corner tile of the small kernel: _mm512_reduce_add_ps order
+#pragma unroll
+      for (int l = 0; l < 8; ++l) s[l] = __fadd_rn(r[l], r[l + 8]);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) u[l] = __fadd_rn(s[l], s[l + 4]);
+      return __fadd_rn(__fadd_rn(u[0], u[2]), __fadd_rn(u[1], u[3]));
+    }
+#pragma unroll
+    for (int l = 0; l < 8; ++l) s[l] = __fadd_rn(r[2 * l], r[2 * l + 1]);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) u[l] = __fadd_rn(s[2 * l], s[2 * l + 1]);
+    return __fadd_rn(__fadd_rn(u[0], u[1]), __fadd_rn(u[2], u[3]));
+  }
+  if (order == AC_ORDER_GEMV8) {
+    float a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = 0.f;
+    for (int t = 0; t < d; ++t) a[t & 7] = __fmaf_rn(gx(t), gc(t), a[t & 7]);
+    float s0 = __fadd_rn(a[0], a[4]), s1 = __fadd_rn(a[1], a[5]);
+    float s2 = __fadd_rn(a[2], a[6]), s3 = __fadd_rn(a[3], a[7]);
+    return __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));
+  }
+  float acc = 0.f;
+  for (int t = 0; t < d; ++t) acc = __fmaf_rn(gx(t), gc(t), acc);
+  return acc;
+}
+
+// d = (xx - 2 xc) + cc, clipped at 0 exactly as np.maximum(d, 0.0)
+AC_DEV float sq_dist(float xx, float xc, float cc) {
+  float d = __fadd_rn(__fsub_rn(xx, __fmul_rn(2.f, xc)), cc);
+  return np_maximum(d, 0.f);
+}
+
+// ---------------------------------------------------------------------------
+// K1: row squared norms and l2 normalisation (tensorops.py:59-76)
+// ---------------------------------------------------------------------------
+__global__ void k_row_sqnorm(const void* __restrict__ x, int dtype, int64_t rows,
+                             int d, float* __restrict__ out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t base = r * d;
+  auto get = [&](int i) {
+    float v = ld_elem(x, dtype, base + i);
+    return __fmul_rn(v, v);
+  };
+  out[r] = pw_sum<float>(get, d);
+}
+
+__global__ void k_l2norm(const void* __restrict__ x, int dtype, int64_t rows, int d,
+                         float* __restrict__ out, float* __restrict__ out_sq,
+                         uint8_t* __restrict__ degenerate) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t base = r * d;
+  auto get = [&](int i) {
+    float v = ld_elem(x, dtype, base + i);
+    return __fmul_rn(v, v);
+  };
+  const float norm = __fsqrt_rn(pw_sum<float>(get, d));
+  const bool degen = norm < 1e-12f;                       // DEGENERATE_NORM
+  const bool unit = fabsf(__fsub_rn(norm, 1.0f)) <= 2e-6f;  // already unit
+  const float safe = (degen || unit) ? 1.0f : norm;
+  for (int i = 0; i < d; ++i) {
+    float v = degen ? 0.f : __fdiv_rn(ld_elem(x, dtype, base + i), safe);
+    out[base + i] = v;
+  }
+  if (degenerate) degenerate[r] = degen ? 1 : 0;
+  if (out_sq) {
+    auto geto = [&](int i) {
+      float v = out[base + i];
+      return __fmul_rn(v, v);
+    };
+    out_sq[r] = pw_sum<float>(geto, d);
+  }
+}
+
+// center squared norms cc[c] for problem blockIdx.y
+__global__ void k_center_sqnorm(const ac_cluster_problem* __restrict__ probs, int d,
+                                int c_lo) {
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  const int c = c_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P.k) return;
+  const float* row = P.centers + (int64_t)c * d;
+  auto get = [&](int i) { return __fmul_rn(row[i], row[i]); };
+  P.cc[c] = pw_sum<float>(get, d);
+}
+
+__global__ void k_problem_xx(const ac_cluster_problem* __restrict__ probs, int dtype,
+                             int d) {
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P.n) return;
+  const int64_t base = r * d;
+  auto get = [&](int i) {
+    float v = ld_elem(P.x, dtype, base + i);
+    return __fmul_rn(v, v);
+  };
+  P.xx[r] = pw_sum<float>(get, d);
+}
+
+__global__ void k_status_init(const ac_cluster_problem* __restrict__ probs, int nprob) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nprob) return;
+  int32_t* st = probs[p].status;
+  st[AC_ST_ACTIVE] = 1;
+  st[AC_ST_NITER] = 0;
+  st[AC_ST_DONE] = 0;
+  st[AC_ST_FLAGS] = 0;
+  st[AC_ST_KPP_STOP] = -1;
+  st[AC_ST_REPAIRS] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// K3: assignment.  x @ centers.T as per-thread sequential fmaf chains
+// (the reference's OpenBLAS general-path order), 128 rows x 64 centres per
+// CTA pass, 8x4 register tile per thread; fused distance + first-index argmin
+// + per-tile label histogram.
+// ---------------------------------------------------------------------------
+constexpr int kAsgBM = 128;
+constexpr int kAsgBN = 64;
+constexpr int kAsgPadM = kAsgBM + 4;
+constexpr int kAsgPadN = kAsgBN + 4;
+
+__host__ __device__ inline size_t assign_smem_bytes(int d, int kcap) {
+  return sizeof(float) * ((size_t)d * kAsgPadM + (size_t)d * kAsgPadN + kAsgBM + kAsgBN +
+                          8 * kAsgBM) +
+         sizeof(int) * (8 * kAsgBM + (size_t)kcap + 4);
+}
+
+__global__ void __launch_bounds__(256)
+k_assign_seq(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int c_lo,
+             int flags, int kcap) {
+  extern __shared__ __align__(16) float smem[];
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  if (!(flags & AC_ASSIGN_ALL) && P.status[AC_ST_ACTIVE] == 0) return;
+  const int64_t n = P.n;
+  const int64_t row0 = (int64_t)blockIdx.x * kAsgBM;
+  if (row0 >= n) return;
+  const int rows = (int)min((int64_t)kAsgBM, n - row0);
+  const int k = P.k;
+
+  float* xs = smem;                       // [d][kAsgPadM]
+  float* cs = xs + (size_t)d * kAsgPadM;  // [d][kAsgPadN]
+  float* s_xx = cs + (size_t)d * kAsgPadN;
+  float* s_cc = s_xx + kAsgBM;
+  float* s_bd = s_cc + kAsgBN;            // [8][kAsgBM]
+  int* s_bi = reinterpret_cast<int*>(s_bd + 8 * kAsgBM);
+  int* s_hist = s_bi + 8 * kAsgBM;        // [kcap]
+
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kAsgBM * d; e += blockDim.x) {
+    const int r = e / d, t = e - r * d;
+    xs[t * kAsgPadM + r] = (r < rows) ? ld_elem(P.x, dtype, (row0 + r) * d + t) : 0.f;
+  }
+  for (int r = tid; r < kAsgBM; r += blockDim.x) s_xx[r] = (r < rows) ? P.xx[row0 + r] : 0.f;
+
+  const int tm = tid & 15;   // rows tm*8 .. tm*8+7
+  const int tn = tid >> 4;   // centres tn*4 .. tn*4+3 of the current 64-block
+  float bd[8];
+  int bi[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { bd[i] = INFINITY; bi[i] = INT_MAX; }
+
+  for (int cb = c_lo; cb < k; cb += kAsgBN) {
+    __syncthreads();
+    const int nc = min(kAsgBN, k - cb);
+    for (int e = tid; e < kAsgBN * d; e += blockDim.x) {
+      const int j = e / d, t = e - j * d;
+      cs[t * kAsgPadN + j] = (j < nc) ? P.centers[(int64_t)(cb + j) * d + t] : 0.f;
+    }
+    for (int j = tid; j < kAsgBN; j += blockDim.x) s_cc[j] = (j < nc) ? P.cc[cb + j] : 0.f;
+    __syncthreads();
+    if (tn * 4 < nc) {
+      float acc[8][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+      const float* xp = xs + tm * 8;
+      const float* cp = cs + tn * 4;
+#pragma unroll 4
+      for (int t = 0; t < d; ++t) {
+        const float4 a0 = *reinterpret_cast<const float4*>(xp + t * kAsgPadM);
+        const float4 a1 = *reinterpret_cast<const float4*>(xp + t * kAsgPadM + 4);
+        const float4 b = *reinterpret_cast<const float4*>(cp + t * kAsgPadN);
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(a[i], bb[j], acc[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xx = s_xx[tm * 8 + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int jj = tn * 4 + j;
+          if (jj < nc) {
+            const float dd = sq_dist(xx, acc[i][j], s_cc[jj]);
+            if (dd < bd[i]) { bd[i] = dd; bi[i] = cb + jj; }
+          }
+        }
+      }
+    }
+  }
+  // merge the 16 centre groups of each row: lanes l and l^16 share tm
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float od = __shfl_xor_sync(0xffffffffu, bd[i], 16);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi[i], 16);
+    argmin_merge(bd[i], bi[i], od, oi);
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  if (lane < 16) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      s_bd[warp * kAsgBM + tm * 8 + i] = bd[i];
+      s_bi[warp * kAsgBM + tm * 8 + i] = bi[i];
+    }
+  }
+  const bool count = !(flags & AC_ASSIGN_MERGE);
+  if (count)
+    for (int c = tid; c < k; c += blockDim.x) s_hist[c] = 0;
+  __syncthreads();
+  if (tid < rows) {
+    float b = s_bd[tid];
+    int l = s_bi[tid];
+    for (int w = 1; w < 8; ++w) argmin_merge(b, l, s_bd[w * kAsgBM + tid], s_bi[w * kAsgBM + tid]);
+    const int64_t r = row0 + tid;
+    if (flags & AC_ASSIGN_MERGE) {
+      const float eb = P.best[r];
+      if (!(b < eb)) { b = eb; l = P.labels[r]; }
+    }
+    if (l == INT_MAX) l = c_lo;  // all-NaN row: numpy argmin returns the first index
+    P.labels[r] = l;
+    P.best[r] = b;
+    if (count) atomicAdd(&s_hist[l], 1);
+  }
+  if (count) {
+    __syncthreads();
+    int32_t* th = P.tile_hist + (int64_t)blockIdx.x * k;
+    for (int c = tid; c < k; c += blockDim.x) th[c] = s_hist[c];
+  }
+}
+
+// Generic-order assignment for the small shapes the reference sends through
+// OpenBLAS's small-matrix / GEMV kernels (M*N <= ~1.2K or a unit dimension).
+// One thread per row; centres staged in shared memory.
+__global__ void k_assign_generic(const ac_cluster_problem* __restrict__ probs, int dtype,
+                                 int d, int c_lo, int flags, int kcap) {
+  extern __shared__ __align__(16) float smem[];
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  if (!(flags & AC_ASSIGN_ALL) && P.status[AC_ST_ACTIVE] == 0) return;
+  const int64_t n = P.n;
+  const int64_t row0 = (int64_t)blockIdx.x * kAsgBM;
+  if (row0 >= n) return;
+  const int k = P.k;
+  int* s_hist = reinterpret_cast<int*>(smem);
+  const bool count = !(flags & AC_ASSIGN_MERGE);
+  if (count)
+    for (int c = threadIdx.x; c < k; c += blockDim.x) s_hist[c] = 0;
+  __syncthreads();
+  const int64_t r = row0 + threadIdx.x;
+  if (threadIdx.x < kAsgBM && r < n) {
+    const int64_t base = r * d;
+    const float xx = P.xx[r];
+    float b = INFINITY;
+    int l = INT_MAX;
+    for (int c = c_lo; c < k; ++c) {
+      const float* crow = P.centers + (int64_t)c * d;
+      const bool halves = (r >= n - n % 4) && (c >= k - k % 4);
+      const float xc = ordered_dot([&](int t) { return ld_elem(P.x, dtype, base + t); },
+                                   [&](int t) { return crow[t]; }, d, P.order, halves);
+      const float dd = sq_dist(xx, xc, P.cc[c]);
+      if (dd < b) { b = dd; l = c; }
+    }
+    if (flags & AC_ASSIGN_MERGE) {
+      const float eb = P.best[r];
+      if (!(b < eb)) { b = eb; l = P.labels[r]; }
+    }
+    if (l == INT_MAX) l = c_lo;
+    P.labels[r] = l;
+    P.best[r] = b;
+    if (count) atomicAdd(&s_hist[l], 1);
+  }
+  if (count) {
+    __syncthreads();
+    int32_t* th = P.tile_hist + (int64_t)blockIdx.x * k;
+    for (int c = threadIdx.x; c < k; c += blockDim.x) th[c] = s_hist[c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stable counting sort by label (np.argsort(labels, kind="stable")):
+//   scan:    per label, exclusive prefix of the per-tile histograms (relative
+//            tile bases) and the label's total count
+//   post:    (one CTA per problem) empty-cluster repair, inertia, starts
+//   scatter: perm[starts[c] + base[tile][c] + rank-in-tile] = row
+// ---------------------------------------------------------------------------
+__global__ void k_hist_scan(const ac_cluster_problem* __restrict__ probs, int flags) {
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  if (!(flags & AC_ASSIGN_ALL) && P.status[AC_ST_ACTIVE] == 0) return;
+  const int k = P.k;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  const int tiles = (int)((P.n + kAsgBM - 1) / kAsgBM);
+  int32_t* h = P.tile_hist + c;
+  int run = 0;
+  int t = 0;
+  for (; t + 4 <= tiles; t += 4) {
+    const int v0 = h[(int64_t)(t + 0) * k], v1 = h[(int64_t)(t + 1) * k];
+    const int v2 = h[(int64_t)(t + 2) * k], v3 = h[(int64_t)(t + 3) * k];
+    h[(int64_t)(t + 0) * k] = run; run += v0;
+    h[(int64_t)(t + 1) * k] = run; run += v1;
+    h[(int64_t)(t + 2) * k] = run; run += v2;
+    h[(int64_t)(t + 3) * k] = run; run += v3;
+  }
+  for (; t < tiles; ++t) {
+    const int v = h[(int64_t)t * k];
+    h[(int64_t)t * k] = run;
+    run += v;
+  }
+  P.counts[c] = run;
+}
+
+// _repair_empty (clustering.py:100-116) + inertia (:132) + segment starts.
+// One CTA (1024 threads) per problem.  `iter` < 0 skips the inertia entry.
+__global__ void __launch_bounds__(1024)
+k_post(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int iter, int flags) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  const ac_cluster_problem& P = probs[blockIdx.x];
+  if (!(flags & AC_ASSIGN_ALL) && P.status[AC_ST_ACTIVE] == 0) return;
+  const int k = P.k;
+  const int64_t n = P.n;
+  const int tid = threadIdx.x;
+  __shared__ int s_empty;
+  __shared__ float s_far_d[32];
+  __shared__ long long s_far_i[32];
+  __shared__ int s_scan[1024];
+
+  // ---- empty-cluster repair: loop to a fixed point, at most k times ----
+  for (int guard = 0; guard < k; ++guard) {
+    if (tid == 0) s_empty = INT_MAX;
+    __syncthreads();
+    for (int c = tid; c < k; c += blockDim.x)
+      if (P.counts[c] == 0) atomicMin(&s_empty, c);
+    __syncthreads();
+    const int c = s_empty;
+    if (c == INT_MAX) break;
+    // far = argmax of the assigned distances (first maximum)
+    float bdv = -INFINITY;
+    long long bix = LLONG_MAX;
+    for (int64_t i = tid; i < n; i += blockDim.x) {
+      const float v = P.best[i];
+      if (v > bdv) { bdv = v; bix = i; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const float od = __shfl_xor_sync(0xffffffffu, bdv, o);
+      const long long oi = __shfl_xor_sync(0xffffffffu, bix, o);
+      if (od > bdv || (od == bdv && oi < bix)) { bdv = od; bix = oi; }
+    }
+    if ((tid & 31) == 0) { s_far_d[tid >> 5] = bdv; s_far_i[tid >> 5] = bix; }
+    __syncthreads();
+    if (tid == 0) {
+      float fd = s_far_d[0];
+      long long fi = s_far_i[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+        if (s_far_d[w] > fd || (s_far_d[w] == fd && s_far_i[w] < fi)) { fd = s_far_d[w]; fi = s_far_i[w]; }
+      s_far_i[0] = fi;
+    }
+    __syncthreads();
+    const int64_t far = s_far_i[0];
+    const int old = P.labels[far];
+    for (int t = tid; t < d; t += blockDim.x)
+      P.centers[(int64_t)c * d + t] = ld_elem(P.x, dtype, far * d + t);
+    __syncthreads();
+    if (tid == 0) {
+      P.labels[far] = c;
+      P.best[far] = 0.f;  // ((x[far] - x[far])**2).sum() == 0
+      P.counts[c] += 1;
+      P.counts[old] -= 1;
+      P.status[AC_ST_REPAIRS] += 1;
+    }
+    // relative tile bases: tiles after far's tile see one fewer `old`, one more `c`
+    const int tiles = (int)((n + kAsgBM - 1) / kAsgBM);
+    const int ft = (int)(far / kAsgBM);
+    for (int t = ft + 1 + tid; t < tiles; t += blockDim.x) {
+      P.tile_hist[(int64_t)t * k + old] -= 1;
+      P.tile_hist[(int64_t)t * k + c] += 1;
+    }
+    __syncthreads();
+  }
+
+  // ---- inertia_history entry: float(d[arange(n), labels].sum()) ----
+  if (iter >= 0) {
+    PwPlan plan{P.plan_n};
+    float* vals = reinterpret_cast<float*>(psm);
+    const float* best = P.best;
+    const float s = pw_eval_block<float>(plan, [&](int i) { return best[i]; }, vals);
+    if (tid == 0) P.inertia[iter] = s;
+  }
+
+  // ---- starts = exclusive scan of counts (k <= 1024 * chunk) ----
+  const int per = (k + blockDim.x - 1) / blockDim.x;
+  int local = 0;
+  for (int j = 0; j < per; ++j) {
+    const int c = tid * per + j;
+    if (c < k) local += P.counts[c];
+  }
+  s_scan[tid] = local;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+    const int v = (tid >= off) ? s_scan[tid - off] : 0;
+    __syncthreads();
+    s_scan[tid] += v;
+    __syncthreads();
+  }
+  int run = s_scan[tid] - local;
+  for (int j = 0; j < per; ++j) {
+    const int c = tid * per + j;
+    if (c < k) { P.starts[c] = run; run += P.counts[c]; }
+  }
+  if (tid == blockDim.x - 1) P.starts[k] = s_scan[tid];
+}
+
+__global__ void k_scatter(const ac_cluster_problem* __restrict__ probs, int flags) {
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  if (!(flags & AC_ASSIGN_ALL) && P.status[AC_ST_ACTIVE] == 0) return;
+  const int64_t row0 = (int64_t)blockIdx.x * kAsgBM;
+  if (row0 >= P.n) return;
+  const int rows = (int)min((int64_t)kAsgBM, P.n - row0);
+  __shared__ int s_lab[kAsgBM];
+  const int tid = threadIdx.x;
+  if (tid < rows) s_lab[tid] = P.labels[row0 + tid];
+  __syncthreads();
+  if (tid < rows) {
+    const int l = s_lab[tid];
+    int rank = 0;
+    for (int j = 0; j < tid; ++j) rank += (s_lab[j] == l);
+    const int pos = P.starts[l] + P.tile_hist[(int64_t)blockIdx.x * P.k + l] + rank;
+    P.perm[pos] = (int32_t)(row0 + tid);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: centroid update (clustering.py:133-143).  One warp per centre: the f64
+// sum runs over the members in stable label order exactly like
+// np.add.reduceat(x[order].astype(f64), starts), then / count -> f32.
+// The same warp computes the f32 movement norm and the new ||c||^2; the last
+// warp of a problem reduces the movement mean and clears the active flag when
+// movement < tol.
+// ---------------------------------------------------------------------------
+constexpr int kMaxDimPerLane = 8;  // D <= 256
+
+__global__ void __launch_bounds__(256)
+k_update(const ac_cluster_problem* __restrict__ probs, int dtype, int d, double tol,
+         int mode /*0 = lloyd update, 1 = segment mean into out*/, float* const* outs) {
+  extern __shared__ __align__(16) float usm[];
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  if (mode == 0 && P.status[AC_ST_ACTIVE] == 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + warp;
+  const int k = P.k;
+  float* sq = usm + warp * 2 * d;  // [2][d] scratch per warp
+  const bool valid = c < k;
+  if (valid) {
+    const int cnt = P.counts[c];
+    const int s0 = P.starts[c];
+    double acc[kMaxDimPerLane];
+#pragma unroll
+    for (int j = 0; j < kMaxDimPerLane; ++j) acc[j] = 0.0;
+    const int nper = (d + 31) >> 5;
+    // first member initialises (reduceat copies the first row), the rest add in order
+    int m = 0;
+    constexpr int U = 4;
+    for (; m + U <= cnt; m += U) {
+      int64_t rows[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) rows[u] = P.perm[s0 + m + u];
+      float v[U][kMaxDimPerLane];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < kMaxDimPerLane; ++j) {
+          const int t = lane + 32 * j;
+          v[u][j] = (j < nper && t < d) ? ld_elem(P.x, dtype, rows[u] * d + t) : 0.f;
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < kMaxDimPerLane; ++j)
+          acc[j] = (m + u == 0) ? (double)v[u][j] : __dadd_rn(acc[j], (double)v[u][j]);
+    }
+    for (; m < cnt; ++m) {
+      const int64_t row = P.perm[s0 + m];
+#pragma unroll
+      for (int j = 0; j < kMaxDimPerLane; ++j) {
+        const int t = lane + 32 * j;
+        const float v = (j < nper && t < d) ? ld_elem(P.x, dtype, row * d + t) : 0.f;
+        acc[j] = (m == 0) ? (double)v : __dadd_rn(acc[j], (double)v);
+      }
+    }
+    const double dc = (double)cnt;
+    float* dst = (mode == 0) ? P.centers + (int64_t)c * d : outs[blockIdx.y] + (int64_t)c * d;
+#pragma unroll
+    for (int j = 0; j < kMaxDimPerLane; ++j) {
+      const int t = lane + 32 * j;
+      if (j < nper && t < d) {
+        const float nv = __double2float_rn(__ddiv_rn(acc[j], dc));
+        if (mode == 0) {
+          const float ov = dst[t];
+          const float df = __fsub_rn(nv, ov);
+          sq[t] = __fmul_rn(df, df);
+          sq[d + t] = __fmul_rn(nv, nv);
+        }
+        dst[t] = nv;
+      }
+    }
+    __syncwarp();
+    if (mode == 0 && lane == 0) {
+      const float* a = sq;
+      const float* b = sq + d;
+      P.movement[c] = __fsqrt_rn(pw_sum<float>([&](int i) { return a[i]; }, d));
+      P.cc[c] = pw_sum<float>([&](int i) { return b[i]; }, d);
+    }
+  }
+  if (mode != 0) return;
+  // completion counting per problem (one arrival per warp that owns a centre)
+  __shared__ int s_last[8];
+  if (lane == 0) {
+    s_last[warp] = 0;
+    if (valid) {
+      __threadfence();
+      const int prev = atomicAdd(&P.status[AC_ST_DONE], 1);
+      s_last[warp] = (prev == k - 1);
+    }
+  }
+  __syncwarp();
+  if (valid && s_last[warp] && lane == 0) {
+    __threadfence();
+    const volatile float* mv = P.movement;
+    const float s = pw_sum<float>([&](int i) { return mv[i]; }, k);
+    const float mean = __double2float_rn(__ddiv_rn((double)s, (double)k));
+    P.status[AC_ST_DONE] = 0;
+    P.status[AC_ST_NITER] += 1;
+    if ((double)mean < tol) P.status[AC_ST_ACTIVE] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: k-means++ seeding (clustering.py:78-91)
+// ---------------------------------------------------------------------------
+__global__ void k_kpp_init(const ac_cluster_problem* __restrict__ probs, int dtype, int d,
+                           const double* __restrict__ draws, int max_k) {
+  const ac_cluster_problem& P = probs[blockIdx.x];
+  const int64_t first = (int64_t)draws[(int64_t)blockIdx.x * max_k];
+  for (int t = threadIdx.x; t < d; t += blockDim.x)
+    P.centers[t] = ld_elem(P.x, dtype, first * d + t);
+}
+
+// closest = min(closest, ((x - centers[s]) ** 2).sum(axis=1))  (s == 0: assign)
+__global__ void k_kpp_dist(const ac_cluster_problem* __restrict__ probs, int dtype, int d,
+                           int s) {
+  extern __shared__ __align__(16) float ksm[];
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  if (s + 1 >= P.k || P.status[AC_ST_KPP_STOP] >= 0) return;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) ksm[t] = P.centers[(int64_t)s * d + t];
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P.n) return;
+  const int64_t base = r * d;
+  auto get = [&](int i) {
+    const float df = __fsub_rn(ld_elem(P.x, dtype, base + i), ksm[i]);
+    return __fmul_rn(df, df);
+  };
+  const float dist = pw_sum<float>(get, d);
+  P.best[r] = (s == 0) ? dist : np_minimum(P.best[r], dist);
+}
+
+// total = closest.sum(); p = closest / total; choice(n, p): f64 cumsum,
+// /= cdf[-1], searchsorted(u, 'right').  One CTA of 1024 threads per problem.
+// The f64 prefix sums are computed in parallel; they equal numpy's sequential
+// cumsum exactly whenever every non-zero p >= 2^-29 (all partial sums are then
+// multiples of 2^-52 below 2, hence exact) — otherwise a single thread replays
+// the sequential cumsum.
+__global__ void __launch_bounds__(1024)
+k_kpp_pick(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int s,
+           const double* __restrict__ draws, int max_k) {
+  extern __shared__ __align__(16) unsigned char kpsm[];
+  const ac_cluster_problem& P = probs[blockIdx.x];
+  if (s + 1 >= P.k || P.status[AC_ST_KPP_STOP] >= 0) return;
+  const int64_t n = P.n;
+  const int tid = threadIdx.x;
+  const float* closest = P.best;
+  PwPlan plan{P.plan_n};
+  const float total =
+      pw_eval_block<float>(plan, [&](int i) { return closest[i]; }, reinterpret_cast<float*>(kpsm));
+  const double draw = draws[(int64_t)blockIdx.x * max_k + s + 1];
+  __shared__ long long s_idx;
+  __shared__ int s_inexact;
+  __shared__ double s_pref[1024];
+  __shared__ int s_first;
+  if (!(total > 0.f)) {
+    // `if total <= 0: idx = int(rng.integers(n))` — forced draw or stop
+    if (tid == 0) {
+      if (draw < 0) s_idx = (long long)(-draw) - 1;
+      else { s_idx = -1; P.status[AC_ST_KPP_STOP] = s + 1; }
+    }
+    __syncthreads();
+  } else {
+    if (tid == 0) { s_inexact = 0; s_first = INT_MAX; }
+    __syncthreads();
+    const int64_t seg = (n + blockDim.x - 1) / blockDim.x;
+    const int64_t lo = min(n, (int64_t)tid * seg), hi = min(n, lo + seg);
+    double local = 0.0;
+    int inexact = 0;
+    for (int64_t j = lo; j < hi; ++j) {
+      const float p = __fdiv_rn(closest[j], total);
+      if (p != 0.f && p < 1.8626451e-09f) inexact = 1;  // 2^-29
+      local = __dadd_rn(local, (double)p);
+    }
+    if (inexact) s_inexact = 1;
+    s_pref[tid] = local;
+    __syncthreads();
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+      const double v = (tid >= off) ? s_pref[tid - off] : 0.0;
+      __syncthreads();
+      s_pref[tid] = __dadd_rn(s_pref[tid], v);
+      __syncthreads();
+    }
+    const double last = s_pref[blockDim.x - 1];
+    const double u = draw;
+    if (!s_inexact) {
+      if (hi > lo && __ddiv_rn(s_pref[tid], last) > u) atomicMin(&s_first, tid);
+      __syncthreads();
+      if (tid == s_first) {
+        double run = s_pref[tid] - local;  // exact: all partial sums representable
+        long long idx = hi;
+        for (int64_t j = lo; j < hi; ++j) {
+          run = __dadd_rn(run, (double)__fdiv_rn(closest[j], total));
+          if (__ddiv_rn(run, last) > u) { idx = j; break; }
+        }
+        s_idx = idx;
+      }
+      if (tid == 0 && s_first == INT_MAX) s_idx = n;  // u beyond the cdf (cannot happen)
+      __syncthreads();
+    } else {
+      if (tid == 0) {
+        // sequential replay of numpy's cumsum
+        double run = 0.0;
+        for (int64_t j = 0; j < n; ++j) run = __dadd_rn(run, (double)__fdiv_rn(closest[j], total));
+        const double lastv = run;
+        run = 0.0;
+        long long idx = n;
+        for (int64_t j = 0; j < n; ++j) {
+          run = __dadd_rn(run, (double)__fdiv_rn(closest[j], total));
+          if (__ddiv_rn(run, lastv) > u) { idx = j; break; }
+        }
+        s_idx = idx;
+        P.status[AC_ST_FLAGS] |= 1;  // sequential cumsum fallback used
+      }
+      __syncthreads();
+    }
+  }
+  const long long idx = s_idx;
+  if (idx < 0) return;
+  const int64_t ci = min((long long)n - 1, idx);
+  for (int t = tid; t < d; t += blockDim.x)
+    P.centers[(int64_t)(s + 1) * d + t] = ld_elem(P.x, dtype, ci * d + t);
+}
+
+// ---------------------------------------------------------------------------
+// multi-stage helpers
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024)
+k_reduce_best(const ac_cluster_problem* __restrict__ probs, float* sum_out, float* mean_out) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  const ac_cluster_problem& P = probs[blockIdx.x];
+  const float* best = P.best;
+  PwPlan plan{P.plan_n};
+  const float s = pw_eval_block<float>(plan, [&](int i) { return best[i]; },
+                                       reinterpret_cast<float*>(rsm));
+  if (threadIdx.x == 0) {
+    if (sum_out) sum_out[blockIdx.x] = s;
+    if (mean_out) mean_out[blockIdx.x] = __double2float_rn(__ddiv_rn((double)s, (double)P.n));
+  }
+}
+
+// per-row f64 distance to the assigned centre; sqrt_it: norm (tau) or squared (mse)
+__global__ void k_row_dist_f64(const ac_cluster_problem* __restrict__ probs, int dtype, int d,
+                               int sqrt_it) {
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P.n) return;
+  const int64_t base = r * d;
+  const float* crow = P.centers + (int64_t)P.labels[r] * d;
+  auto get = [&](int i) {
+    const double df = __dsub_rn((double)ld_elem(P.x, dtype, base + i), (double)crow[i]);
+    return __dmul_rn(df, df);
+  };
+  const double s = pw_sum<double>(get, d);
+  P.dscratch[r] = sqrt_it ? __dsqrt_rn(s) : s;
+}
+
+__global__ void __launch_bounds__(1024)
+k_reduce_dscratch(const ac_cluster_problem* __restrict__ probs, double factor, double* out) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const ac_cluster_problem& P = probs[blockIdx.x];
+  const double* v = P.dscratch;
+  PwPlan plan{P.plan_n};
+  const double s = pw_eval_block<double>(plan, [&](int i) { return v[i]; },
+                                         reinterpret_cast<double*>(dsm));
+  if (threadIdx.x == 0) out[blockIdx.x] = __dmul_rn(factor, __ddiv_rn(s, (double)P.n));
+}
+
+// retire distances: keep[i] = ||x_i - c[label_i]|| (f32) >= tau32
+__global__ void k_retire_flags(const ac_cluster_problem* __restrict__ probs, int dtype, int d,
+                               const float* __restrict__ tau32) {
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P.n) return;
+  const int64_t base = r * d;
+  const float* crow = P.centers + (int64_t)P.labels[r] * d;
+  auto get = [&](int i) {
+    const float df = __fsub_rn(ld_elem(P.x, dtype, base + i), crow[i]);
+    return __fmul_rn(df, df);
+  };
+  const float dist = __fsqrt_rn(pw_sum<float>(get, d));
+  reinterpret_cast<uint8_t*>(P.dscratch)[r] = (dist >= tau32[blockIdx.y]) ? 1 : 0;
+}
+
+// order-preserving compaction of idx_in by the keep flags; one CTA per problem
+__global__ void __launch_bounds__(1024)
+k_retire_compact(const ac_cluster_problem* __restrict__ probs, const int64_t* const* idx_in,
+                 int64_t* const* idx_out, int64_t* out_count) {
+  const ac_cluster_problem& P = probs[blockIdx.x];
+  const int64_t n = P.n;
+  const uint8_t* keep = reinterpret_cast<const uint8_t*>(P.dscratch);
+  const int tid = threadIdx.x;
+  const int64_t seg = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t lo = min(n, (int64_t)tid * seg), hi = min(n, lo + seg);
+  __shared__ long long s_sc[1024];
+  long long local = 0;
+  for (int64_t i = lo; i < hi; ++i) local += keep[i];
+  s_sc[tid] = local;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+    const long long v = (tid >= off) ? s_sc[tid - off] : 0;
+    __syncthreads();
+    s_sc[tid] += v;
+    __syncthreads();
+  }
+  long long pos = s_sc[tid] - local;
+  const int64_t* in = idx_in[blockIdx.x];
+  int64_t* out = idx_out[blockIdx.x];
+  for (int64_t i = lo; i < hi; ++i)
+    if (keep[i]) out[pos++] = in[i];
+  if (tid == blockDim.x - 1) out_count[blockIdx.x] = s_sc[tid];
+}
+
+__global__ void k_gather_rows(const void* __restrict__ src, int dtype, int d,
+                              const int64_t* __restrict__ idx, int64_t rows,
+                              void* __restrict__ dst) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * d) return;
+  const int64_t r = e / d, t = e - r * d;
+  const int64_t s = idx[r] * d + t;
+  if (dtype == AC_DTYPE_BF16)
+    reinterpret_cast<__nv_bfloat16*>(dst)[e] = reinterpret_cast<const __nv_bfloat16*>(src)[s];
+  else
+    reinterpret_cast<float*>(dst)[e] = reinterpret_cast<const float*>(src)[s];
+}
+
+// drop centres without members (clustering.py:303-310).  One CTA per problem.
+__global__ void __launch_bounds__(1024)
+k_drop_empty(const ac_cluster_problem* __restrict__ probs, int d, int32_t* new_k) {
+  const ac_cluster_problem& P = probs[blockIdx.x];
+  const int k = P.k;
+  const int64_t n = P.n;
+  const int tid = threadIdx.x;
+  for (int c = tid; c < k; c += blockDim.x) P.counts[c] = 0;
+  __syncthreads();
+  for (int64_t i = tid; i < n; i += blockDim.x) atomicAdd(&P.counts[P.labels[i]], 1);
+  __syncthreads();
+  // remap: serial prefix over k (k <= a few thousand) by thread 0 into starts[]
+  int32_t* remap = P.starts;
+  if (tid == 0) {
+    int j = 0;
+    for (int c = 0; c < k; ++c) remap[c] = (P.counts[c] > 0) ? j++ : -1;
+    new_k[blockIdx.x] = j;
+  }
+  __syncthreads();
+  // compact centres and counts in increasing order (remap[c] <= c, so row c is
+  // read before any later write can touch it)
+  for (int c = 0; c < k; ++c) {
+    const int j = remap[c];
+    if (j >= 0 && j != c) {
+      for (int t = tid; t < d; t += blockDim.x)
+        P.centers[(int64_t)j * d + t] = P.centers[(int64_t)c * d + t];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    for (int c = 0; c < k; ++c) {
+      const int j = remap[c];
+      if (j >= 0) P.counts[j] = P.counts[c];
+    }
+  }
+  __syncthreads();
+  for (int64_t i = tid; i < n; i += blockDim.x) P.labels[i] = remap[P.labels[i]];
+}
+
+// ---------------------------------------------------------------------------
+// K9: envelopes (quest.py:61-71) — sequential np.maximum/np.minimum over the
+// members in label order, one warp per cluster.
+// ---------------------------------------------------------------------------
+__global__ void k_envelopes(const ac_cluster_problem* __restrict__ probs, int dtype, int d,
+                            float* const* env_max, float* const* env_min) {
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (c >= P.k) return;
+  const int cnt = P.counts[c], s0 = P.starts[c];
+  float* mx = env_max[blockIdx.y] + (int64_t)c * d;
+  float* mn = env_min[blockIdx.y] + (int64_t)c * d;
+  for (int t0 = 0; t0 < d; t0 += 32) {
+    const int t = t0 + lane;
+    if (t >= d) break;
+    float a = 0.f, b = 0.f;
+    for (int m = 0; m < cnt; ++m) {
+      const float v = ld_elem(P.x, dtype, (int64_t)P.perm[s0 + m] * d + t);
+      if (m == 0) { a = v; b = v; }
+      else { a = np_maximum(a, v); b = np_minimum(b, v); }
+    }
+    mx[t] = a;
+    mn[t] = b;
+  }
+}
+
+}  // namespace ac
+
+// ===========================================================================
+// host side
+// ===========================================================================
+using namespace ac;
+
+namespace {
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int set_smem(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return ac_host::check_cuda(e, "cudaFuncSetAttribute");
+  }
+  return AC_OK;
+}
+size_t plan_vals_bytes(int64_t n, size_t elem) {
+  // for n > 128 every leaf holds >= 57 elements (n2 >= n/2 - 7 >= 57), so
+  // leaves <= n/56 + 1; internal nodes = leaves - 1
+  const int64_t L = n <= 128 ? 1 : n / 56 + 2;
+  return (size_t)(2 * L + 2) * elem;
+}
+}  // namespace
+
+extern "C" int ac_row_sqnorm(const void* x, int dtype, int64_t rows, int d, float* out,
+                             void* stream) {
+  if (rows < 0 || d < 1) { ac_host::set_error("ac_row_sqnorm: bad shape"); return AC_ERR_DIM; }
+  if (rows == 0) return AC_OK;
+  k_row_sqnorm<<<(unsigned)((rows + 255) / 256), 256, 0, S(stream)>>>(x, dtype, rows, d, out);
+  AC_CHECK_LAUNCH("k_row_sqnorm");
+  return AC_OK;
+}
+
+extern "C" int ac_l2norm(const void* x, int dtype, int64_t rows, int d, float* out,
+                         float* out_sq, uint8_t* degenerate, void* stream) {
+  if (rows < 0 || d < 1) { ac_host::set_error("ac_l2norm: bad shape"); return AC_ERR_DIM; }
+  if (rows == 0) return AC_OK;
+  k_l2norm<<<(unsigned)((rows + 127) / 128), 128, 0, S(stream)>>>(x, dtype, rows, d, out, out_sq,
+                                                                   degenerate);
+  AC_CHECK_LAUNCH("k_l2norm");
+  return AC_OK;
+}
+
+extern "C" int ac_lloyd_prepare(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                                int64_t max_n, int max_k, void* stream) {
+  if (nprob <= 0) return AC_OK;
+  k_status_init<<<(nprob + 127) / 128, 128, 0, S(stream)>>>(probs, nprob);
+  k_problem_xx<<<dim3((unsigned)((max_n + 255) / 256), nprob), 256, 0, S(stream)>>>(probs, dtype, d);
+  k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, S(stream)>>>(probs, d, 0);
+  AC_CHECK_LAUNCH("ac_lloyd_prepare");
+  return AC_OK;
+}
+
+// `generic` is decided per batch by the host (every problem of a batch shares
+// one accumulation order; the host splits batches otherwise).
+static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                       int64_t max_n, int max_k, int c_lo, int flags, int order,
+                       cudaStream_t st) {
+  const unsigned tiles = (unsigned)((max_n + kAsgBM - 1) / kAsgBM);
+  if (order == AC_ORDER_SEQ) {
+    const size_t smem = assign_smem_bytes(d, max_k);
+    int rc = set_smem((const void*)k_assign_seq, smem);
+    if (rc) return rc;
+    k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
+    k_assign_seq<<<dim3(tiles, nprob), 256, smem, st>>>(probs, dtype, d, c_lo, flags, max_k);
+  } else {
+    const size_t smem = sizeof(int) * (size_t)(max_k + 4);
+    int rc = set_smem((const void*)k_assign_generic, smem);
+    if (rc) return rc;
+    k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
+    k_assign_generic<<<dim3(tiles, nprob), kAsgBM, smem, st>>>(probs, dtype, d, c_lo, flags, max_k);
+  }
+  AC_CHECK_LAUNCH("ac_assign");
+  return AC_OK;
+}
+
+extern "C" int ac_assign_ordered(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                                 int64_t max_n, int max_k, int c_lo, int flags, int order,
+                                 void* stream) {
+  if (nprob <= 0 || max_n <= 0) return AC_OK;
+  if (d < 1 || d > 256) { ac_host::set_error("assign: d=%d unsupported (1..256)", d); return AC_ERR_DIM; }
+  return assign_impl(probs, nprob, dtype, d, max_n, max_k, c_lo, flags, order, S(stream));
+}
+
+extern "C" int ac_assign(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                         int64_t max_n, int max_k, int c_lo, int flags, void* stream) {
+  return ac_assign_ordered(probs, nprob, dtype, d, max_n, max_k, c_lo, flags, AC_ORDER_SEQ, stream);
+}
+
+static int repair_sort_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                            int64_t max_n, int max_k, int iter, int flags, cudaStream_t st) {
+  const unsigned tiles = (unsigned)((max_n + kAsgBM - 1) / kAsgBM);
+  k_hist_scan<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, flags);
+  const size_t psm = plan_vals_bytes(max_n, sizeof(float));
+  int rc = set_smem((const void*)k_post, psm);
+  if (rc) return rc;
+  k_post<<<nprob, 1024, psm, st>>>(probs, dtype, d, iter, flags);
+  k_scatter<<<dim3(tiles, nprob), kAsgBM, 0, st>>>(probs, flags);
+  AC_CHECK_LAUNCH("ac_repair_sort");
+  return AC_OK;
+}
+
+extern "C" int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                              int64_t max_n, int max_k, int iter, int flags, void* stream) {
+  if (nprob <= 0 || max_n <= 0) return AC_OK;
+  return repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, iter, flags, S(stream));
+}
+
+static int update_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d, int max_k,
+                       double tol, int mode, float* const* outs, cudaStream_t st) {
+  const int warps = 8;
+  const size_t smem = sizeof(float) * warps * 2 * d;
+  int rc = set_smem((const void*)k_update, smem);
+  if (rc) return rc;
+  k_update<<<dim3((max_k + warps - 1) / warps, nprob), warps * 32, smem, st>>>(probs, dtype, d, tol,
+                                                                               mode, outs);
+  AC_CHECK_LAUNCH("k_update");
+  return AC_OK;
+}
+
+extern "C" int ac_segment_mean(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                               int max_k, float* const* out, void* stream) {
+  if (nprob <= 0) return AC_OK;
+  return update_impl(probs, nprob, dtype, d, max_k, 0.0, 1, out, S(stream));
+}
+
+extern "C" int ac_lloyd(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                        int64_t max_n, int max_k, int max_iter, double tol, int poll_every,
+                        const ac_cluster_problem* host_probs, void* stream) {
+  if (nprob <= 0) return AC_OK;
+  if (d < 1 || d > 256) { ac_host::set_error("lloyd: d=%d unsupported (1..256)", d); return AC_ERR_DIM; }
+  if (max_k > 16384) { ac_host::set_error("lloyd: k=%d too large", max_k); return AC_ERR_PARAM; }
+  cudaStream_t st = S(stream);
+  // every problem of a batch must share the accumulation order
+  int order = AC_ORDER_SEQ;
+  if (host_probs) order = host_probs[0].order;
+  int rc = ac_lloyd_prepare(probs, nprob, dtype, d, max_n, max_k, stream);
+  if (rc) return rc;
+  int32_t* pinned = nullptr;
+  if (poll_every > 0 && host_probs) cudaMallocHost(&pinned, sizeof(int32_t) * nprob);
+  for (int it = 0; it < max_iter; ++it) {
+    if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, 0, order, st))) break;
+    if ((rc = repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, it, 0, st))) break;
+    if ((rc = update_impl(probs, nprob, dtype, d, max_k, tol, 0, nullptr, st))) break;
+    if (pinned && (it + 1) % poll_every == 0 && it + 1 < max_iter) {
+      for (int p = 0; p < nprob; ++p)
+        cudaMemcpyAsync(pinned + p, host_probs[p].status + AC_ST_ACTIVE, sizeof(int32_t),
+                        cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      int any = 0;
+      for (int p = 0; p < nprob; ++p) any |= pinned[p];
+      if (!any) break;
+    }
+  }
+  if (pinned) cudaFreeHost(pinned);
+  if (rc) return rc;
+  if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, AC_ASSIGN_ALL, order, st))) return rc;
+  return repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, -1, AC_ASSIGN_ALL, st);
+}
+
+extern "C" int ac_kmeanspp(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                           int64_t max_n, int max_k, const double* draws, void* stream) {
+  if (nprob <= 0) return AC_OK;
+  cudaStream_t st = S(stream);
+  k_status_init<<<(nprob + 127) / 128, 128, 0, st>>>(probs, nprob);
+  k_kpp_init<<<nprob, 128, 0, st>>>(probs, dtype, d, draws, max_k);
+  const size_t psm = plan_vals_bytes(max_n, sizeof(float));
+  int rc = set_smem((const void*)k_kpp_pick, psm);
+  if (rc) return rc;
+  for (int s = 0; s + 1 < max_k; ++s) {
+    k_kpp_dist<<<dim3((unsigned)((max_n + 255) / 256), nprob), 256, sizeof(float) * d, st>>>(
+        probs, dtype, d, s);
+    k_kpp_pick<<<nprob, 1024, psm, st>>>(probs, dtype, d, s, draws, max_k);
+  }
+  AC_CHECK_LAUNCH("ac_kmeanspp");
+  return AC_OK;
+}
+
+extern "C" int ac_reduce_best(const ac_cluster_problem* probs, int nprob, int64_t max_n,
+                              float* sum_out, float* mean_out, void* stream) {
+  if (nprob <= 0) return AC_OK;
+  const size_t psm = plan_vals_bytes(max_n, sizeof(float));
+  int rc = set_smem((const void*)k_reduce_best, psm);
+  if (rc) return rc;
+  k_reduce_best<<<nprob, 1024, psm, S(stream)>>>(probs, sum_out, mean_out);
+  AC_CHECK_LAUNCH("k_reduce_best");
+  return AC_OK;
+}
+
+extern "C" int ac_tau(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                      int64_t max_n, double factor, double* tau_out, void* stream) {
+  if (nprob <= 0) return AC_OK;
+  cudaStream_t st = S(stream);
+  k_row_dist_f64<<<dim3((unsigned)((max_n + 255) / 256), nprob), 256, 0, st>>>(probs, dtype, d, 1);
+  const size_t psm = plan_vals_bytes(max_n, sizeof(double));
+  int rc = set_smem((const void*)k_reduce_dscratch, psm);
+  if (rc) return rc;
+  k_reduce_dscratch<<<nprob, 1024, psm, st>>>(probs, factor, tau_out);
+  AC_CHECK_LAUNCH("ac_tau");
+  return AC_OK;
+}
+
+extern "C" int ac_mse_f64(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                          int64_t max_n, double* out, void* stream) {
+  if (nprob <= 0) return AC_OK;
+  cudaStream_t st = S(stream);
+  k_row_dist_f64<<<dim3((unsigned)((max_n + 255) / 256), nprob), 256, 0, st>>>(probs, dtype, d, 0);
+  const size_t psm = plan_vals_bytes(max_n, sizeof(double));
+  int rc = set_smem((const void*)k_reduce_dscratch, psm);
+  if (rc) return rc;
+  k_reduce_dscratch<<<nprob, 1024, psm, st>>>(probs, 1.0, out);
+  AC_CHECK_LAUNCH("ac_mse_f64");
+  return AC_OK;
+}
+
+extern "C" int ac_retire(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                         int64_t max_n, const float* tau32, const int64_t* const* idx_in,
+                         int64_t* const* idx_out, int64_t* out_count, void* stream) {
+  if (nprob <= 0) return AC_OK;
+  cudaStream_t st = S(stream);
+  k_retire_flags<<<dim3((unsigned)((max_n + 255) / 256), nprob), 256, 0, st>>>(probs, dtype, d, tau32);
+  k_retire_compact<<<nprob, 1024, 0, st>>>(probs, idx_in, idx_out, out_count);
+  AC_CHECK_LAUNCH("ac_retire");
+  return AC_OK;
+}
+
+extern "C" int ac_gather_rows(const void* src, int dtype, int d, const int64_t* idx,
+                              int64_t rows, void* dst, void* stream) {
+  if (rows <= 0) return AC_OK;
+  const int64_t total = rows * d;
+  k_gather_rows<<<(unsigned)((total + 255) / 256), 256, 0, S(stream)>>>(src, dtype, d, idx, rows, dst);
+  AC_CHECK_LAUNCH("k_gather_rows");
+  return AC_OK;
+}
+
+extern "C" int ac_drop_empty(const ac_cluster_problem* probs, int nprob, int d, int64_t max_n,
+                             int max_k, int32_t* new_k, void* stream) {
+  if (nprob <= 0) return AC_OK;
+  k_drop_empty<<<nprob, 1024, 0, S(stream)>>>(probs, d, new_k);
+  AC_CHECK_LAUNCH("k_drop_empty");
+  return AC_OK;
+}
+
+extern "C" int ac_envelopes(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                            int max_k, float* const* env_max, float* const* env_min,
+                            void* stream) {
+  if (nprob <= 0) return AC_OK;
+  k_envelopes<<<dim3((max_k + 7) / 8, nprob), 256, 0, S(stream)>>>(probs, dtype, d, env_max, env_min);
+  AC_CHECK_LAUNCH("k_envelopes");
+  return AC_OK;
+}

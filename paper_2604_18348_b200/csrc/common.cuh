@@ -1,0 +1,106 @@
+// Shared device helpers for the AdaCluster sm_100a kernels.
+//
+// Everything on the clustering / selection path must reproduce the reference's
+// numpy + OpenBLAS arithmetic bit-for-bit, so these
+// files are compiled with --fmad=false and every fused multiply-add that the
+// reference performs is written explicitly with __fmaf_rn.  The attention
+// kernels live in separate translation units that allow contraction.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/adacluster_sm100.h"
+
+#define AC_DEV __device__ __forceinline__
+
+namespace ac {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------
+// element loads: the clustering path reads keys either as f32 or as bf16
+// (bf16 -> f32 is exact, so the arithmetic on the upcast values is identical
+// to the oracle's arithmetic on the f32 copy).
+// ---------------------------------------------------------------------------
+AC_DEV float ld_elem(const void* base, int dtype, int64_t i) {
+  if (dtype == AC_DTYPE_BF16) {
+    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[i]);
+  }
+  return reinterpret_cast<const float*>(base)[i];
+}
+
+// ---------------------------------------------------------------------------
+// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum): n < 8 -> sequential from 0; n <= 128 -> 8 strided
+// accumulators combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the tail;
+// otherwise split at n2 = n/2 - (n/2 % 8) and recurse.
+// Used for every `.sum(axis=1)` and `np.linalg.norm(axis=1)` over D.
+// ---------------------------------------------------------------------------
+template <typename T, typename Get>
+AC_DEV T pw_leaf(const Get& get, int lo, int n) {
+  if (n < 8) {
+    T res = T(0);
+    for (int i = 0; i < n; ++i) res = res + get(lo + i);
+    return res;
+  }
+  T r0 = get(lo + 0), r1 = get(lo + 1), r2 = get(lo + 2), r3 = get(lo + 3);
+  T r4 = get(lo + 4), r5 = get(lo + 5), r6 = get(lo + 6), r7 = get(lo + 7);
+  int i = 8;
+  const int full = n - (n % 8);
+  for (; i < full; i += 8) {
+    r0 = r0 + get(lo + i + 0); r1 = r1 + get(lo + i + 1);
+    r2 = r2 + get(lo + i + 2); r3 = r3 + get(lo + i + 3);
+    r4 = r4 + get(lo + i + 4); r5 = r5 + get(lo + i + 5);
+    r6 = r6 + get(lo + i + 6); r7 = r7 + get(lo + i + 7);
+  }
+  T res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  for (; i < n; ++i) res = res + get(lo + i);
+  return res;
+}
+
+// Arbitrary n (short vectors: D, or k <= a few thousand): the recursion
+// depth is log2(n/128)+1, so plain device recursion is fine.
+template <typename T, typename Get>
+__device__ T pw_sum_rec(const Get& get, int lo, int n) {
+  if (n <= 128) return pw_leaf<T>(get, lo, n);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  T a = pw_sum_rec<T>(get, lo, n2);
+  T b = pw_sum_rec<T>(get, lo + n2, n - n2);
+  return a + b;
+}
+template <typename T, typename Get>
+AC_DEV T pw_sum(const Get& get, int n) {
+  if (n <= 128) return pw_leaf<T>(get, 0, n);
+  return pw_sum_rec<T>(get, 0, n);
+}
+
+AC_DEV float warp_min_f(float v) {
+  for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// (value, index) lexicographic argmin helper: smaller value wins, ties -> smaller index
+AC_DEV void argmin_merge(float& bd, int& bi, float od, int oi) {
+  if (od < bd || (od == bd && oi < bi)) { bd = od; bi = oi; }
+}
+// argmax with ties -> smaller index (numpy argmax returns the first maximum)
+AC_DEV void argmax_merge(float& bd, int64_t& bi, float od, int64_t oi) {
+  if (od > bd || (od == bd && oi < bi)) { bd = od; bi = oi; }
+}
+
+}  // namespace ac
+
+// host-side error reporting shared by every translation unit
+namespace ac_host {
+void set_error(const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* what);
+}  // namespace ac_host
+
+#define AC_CHECK_LAUNCH(what)                                                   \
+  do {                                                                          \
+    cudaError_t _e = cudaGetLastError();                                        \
+    if (_e != cudaSuccess) return ac_host::check_cuda(_e, what);                \
+  } while (0)
