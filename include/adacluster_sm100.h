@@ -59,6 +59,7 @@ extern "C" {
 #define AC_SCORER_QUEST 0   /* quest.py:94   max(Q,0)·maxᵀ + min(Q,0)·minᵀ     */
 #define AC_SCORER_MEAN 1    /* quest.py:119  Q·centersᵀ                        */
 #define AC_SCORER_CLAMPED 2 /* quest.py:106  max(Q,0)·max(C,0)ᵀ + min(Q,0)·min(C,0)ᵀ */
+#define AC_SCORER_GIVEN 3   /* scores supplied in ac_select_problem.scores      */
 
 /* ac_assign flags */
 #define AC_ASSIGN_MERGE 1   /* merge into existing (labels,best) with strict '<'
@@ -103,6 +104,8 @@ typedef struct ac_cluster_problem {
 /* ---- library ---------------------------------------------------------- */
 const char* ac_last_error(void);
 int ac_abi_version(void);
+/* sizeof of the three descriptor structs (ABI check for bindings) */
+int ac_struct_sizes(int64_t* out3);
 /* Number of SMs / compute capability of the current device (host query). */
 int ac_device_info(int* sm_count, int* cc_major, int* cc_minor);
 
@@ -158,6 +161,9 @@ int ac_assign_ordered(const ac_cluster_problem* probs, int nprob, int dtype,
 int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dtype,
                    int d, int64_t max_n, int max_k, int iter, int flags,
                    void* stream);
+/* stable member sort of existing labels (no re-assignment): perm/starts/counts */
+int ac_sort_by_label(const ac_cluster_problem* probs, int nprob, int64_t max_n,
+                     int max_k, void* stream);
 /* segment means in f64 over members (clustering.py:134-139, :197-200):
  * out[c] = f32(sum_{i in seg c, member order} f64(x[perm[i]]) / count[c]) */
 int ac_segment_mean(const ac_cluster_problem* probs, int nprob, int dtype,
@@ -229,6 +235,11 @@ typedef struct ac_attn_item {
  * dst[j] = src[perm[j]] for j < n (row gather, 16-byte vectors)            */
 int ac_permute_rows(const void* src, int dtype, int d, const int32_t* perm,
                     int64_t n, void* dst, void* stream);
+
+/* per-head gather: dst[h, j] = src[h, perm[h, j]]; rows of d elements must
+ * be a multiple of 16 bytes (src/dst [heads, L, d], perm [heads, L])       */
+int ac_permute_rows_heads(const void* src, int dtype, int d, const int32_t* perm,
+                          int64_t L, int heads, void* dst, void* stream);
 
 /* Query layout for the attention kernel (pipeline.py:154-165): per head h,
  * every query cluster g becomes a contiguous block of Qp rows padded to a

@@ -23,6 +23,17 @@ __global__ void k_permute_rows16(const uint4* __restrict__ src, const int32_t* _
   dst[e] = src[(int64_t)perm[j] * vec_per_row + part];
 }
 
+// per-head gather: dst[h, j] = src[h, perm[h, j]]
+__global__ void k_permute_rows16_heads(const uint4* __restrict__ src, const int32_t* __restrict__ perm,
+                                       int64_t L, int heads, int vec_per_row, uint4* __restrict__ dst) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)heads * L * vec_per_row) return;
+  const int64_t j = e / vec_per_row;  // global row h*L + jj
+  const int part = (int)(e - j * vec_per_row);
+  const int64_t h = j / L;
+  dst[e] = src[(h * L + perm[j]) * vec_per_row + part];
+}
+
 __global__ void k_permute_rows_b(const uint8_t* __restrict__ src, const int32_t* __restrict__ perm,
                                  int64_t n, int row_bytes, uint8_t* __restrict__ dst) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -260,6 +271,24 @@ extern "C" int ac_permute_rows(const void* src, int dtype, int d, const int32_t*
         reinterpret_cast<const uint8_t*>(src), perm, n, row_bytes, reinterpret_cast<uint8_t*>(dst));
   }
   AC_CHECK_LAUNCH("ac_permute_rows");
+  return AC_OK;
+}
+
+extern "C" int ac_permute_rows_heads(const void* src, int dtype, int d, const int32_t* perm,
+                                     int64_t L, int heads, void* dst, void* stream) {
+  if (L <= 0 || heads <= 0) return AC_OK;
+  const int esz = dtype == AC_DTYPE_BF16 ? 2 : 4;
+  const int row_bytes = d * esz;
+  if (row_bytes % 16 != 0 || ((uintptr_t)src % 16) || ((uintptr_t)dst % 16)) {
+    ac_host::set_error("ac_permute_rows_heads: rows must be 16-byte multiples (d=%d)", d);
+    return AC_ERR_DIM;
+  }
+  const int vpr = row_bytes / 16;
+  const int64_t total = (int64_t)heads * L * vpr;
+  k_permute_rows16_heads<<<(unsigned)((total + 255) / 256), 256, 0,
+                           reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint4*>(src), perm, L, heads, vpr, reinterpret_cast<uint4*>(dst));
+  AC_CHECK_LAUNCH("ac_permute_rows_heads");
   return AC_OK;
 }
 

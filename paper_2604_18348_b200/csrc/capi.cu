@@ -30,6 +30,13 @@ int check_cuda(cudaError_t e, const char* what) {
 extern "C" const char* ac_last_error(void) { return g_last_error.c_str(); }
 extern "C" int ac_abi_version(void) { return AC_ABI_VERSION; }
 
+extern "C" int ac_struct_sizes(int64_t* out3) {
+  out3[0] = (int64_t)sizeof(ac_cluster_problem);
+  out3[1] = (int64_t)sizeof(ac_select_problem);
+  out3[2] = (int64_t)sizeof(ac_attn_item);
+  return AC_OK;
+}
+
 extern "C" int ac_device_info(int* sm_count, int* cc_major, int* cc_minor) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);

@@ -325,6 +325,22 @@ __global__ void k_assign_generic(const ac_cluster_problem* __restrict__ probs, i
   }
 }
 
+// per-tile label histogram from existing labels (sort without re-assigning)
+__global__ void k_tile_hist(const ac_cluster_problem* __restrict__ probs, int kcap) {
+  extern __shared__ __align__(16) int thsm[];
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  const int64_t row0 = (int64_t)blockIdx.x * kAsgBM;
+  if (row0 >= P.n) return;
+  const int rows = (int)min((int64_t)kAsgBM, P.n - row0);
+  const int k = P.k;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) thsm[c] = 0;
+  __syncthreads();
+  if ((int)threadIdx.x < rows) atomicAdd(&thsm[P.labels[row0 + threadIdx.x]], 1);
+  __syncthreads();
+  int32_t* th = P.tile_hist + (int64_t)blockIdx.x * k;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) th[c] = thsm[c];
+}
+
 // ---------------------------------------------------------------------------
 // Stable counting sort by label (np.argsort(labels, kind="stable")):
 //   scan:    per label, exclusive prefix of the per-tile histograms (relative
@@ -1123,4 +1139,18 @@ extern "C" int ac_envelopes(const ac_cluster_problem* probs, int nprob, int dtyp
   k_envelopes<<<dim3((max_k + 7) / 8, nprob), 256, 0, S(stream)>>>(probs, dtype, d, env_max, env_min);
   AC_CHECK_LAUNCH("k_envelopes");
   return AC_OK;
+}
+
+extern "C" int ac_sort_by_label(const ac_cluster_problem* probs, int nprob, int64_t max_n,
+                                int max_k, void* stream) {
+  if (nprob <= 0 || max_n <= 0) return AC_OK;
+  cudaStream_t st = S(stream);
+  const unsigned tiles = (unsigned)((max_n + kAsgBM - 1) / kAsgBM);
+  const size_t smem = sizeof(int) * (size_t)(max_k + 4);
+  int rc = set_smem((const void*)k_tile_hist, smem);
+  if (rc) return rc;
+  k_tile_hist<<<dim3(tiles, nprob), kAsgBM, smem, st>>>(probs, max_k);
+  AC_CHECK_LAUNCH("k_tile_hist");
+  // dtype/d are only used by the (inactive) repair path: counts are all >= 1
+  return repair_sort_impl(probs, nprob, AC_DTYPE_F32, 1, max_n, max_k, -1, AC_ASSIGN_ALL, st);
 }

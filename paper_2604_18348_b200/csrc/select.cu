@@ -72,7 +72,9 @@ k_select(const ac_select_problem* __restrict__ probs, int d, int scorer) {
     const float* ma = P.emax + (int64_t)c * d;
     const float* mi = P.emin + (int64_t)c * d;
     float s;
-    if (scorer == AC_SCORER_MEAN) {
+    if (scorer == AC_SCORER_GIVEN) {
+      s = P.scores[(int64_t)g * C + c];
+    } else if (scorer == AC_SCORER_MEAN) {
       s = sel_dot([&](int t) { return s_q[t]; }, [&](int t) { return ma[t]; }, d, P.order, hv);
     } else if (scorer == AC_SCORER_CLAMPED) {
       const float a = sel_dot([&](int t) { return np_max0(s_q[t]); },
@@ -88,7 +90,7 @@ k_select(const ac_select_problem* __restrict__ probs, int d, int scorer) {
       s = __fadd_rn(a, b);
     }
     s_sc[c] = s;
-    P.scores[(int64_t)g * C + c] = s;
+    if (scorer != AC_SCORER_GIVEN) P.scores[(int64_t)g * C + c] = s;
   }
   __syncthreads();
   // np.argsort(-scores, kind="stable")[:topk]: rank = #greater + #equal-before
@@ -157,7 +159,7 @@ extern "C" int ac_select(const ac_select_problem* probs, int nprob, int d, int s
                          int max_gq, int max_c, int max_topk, void* stream) {
   (void)max_topk;
   if (nprob <= 0) return AC_OK;
-  if (scorer < 0 || scorer > 2) { ac_host::set_error("ac_select: bad scorer %d", scorer); return AC_ERR_PARAM; }
+  if (scorer < 0 || scorer > AC_SCORER_GIVEN) { ac_host::set_error("ac_select: bad scorer %d", scorer); return AC_ERR_PARAM; }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t smem = sizeof(float) * ((size_t)d + max_c) + sizeof(int) * 2 * (size_t)max_c;
   if (smem > 48 * 1024) {

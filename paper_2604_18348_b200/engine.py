@@ -1,0 +1,650 @@
+"""Device-side orchestration of the AdaCluster hot path.
+
+Everything here drives ``libadacluster_sm100.so`` through the C-ABI on the
+current torch CUDA stream.  A *batch* is a set of independent clustering
+problems (the heads of a layer, or one multi-stage round of several heads)
+laid out in a few flat device buffers with one descriptor per problem
+(``ac_cluster_problem``).  Control flow that the reference decides on data
+(Lloyd convergence, empty-cluster repair) stays on the device; the host only
+synchronises where the reference's control flow needs a size it cannot
+bound (multi-stage round sizes, k-means++ ``total <= 0`` replays) or when a
+caller asks for host results.
+
+Reference call sites: clustering.py:78-320, quest.py:61-143,
+pipeline.py:154-275.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .errors import DimensionError, ParameterError
+
+F32 = torch.float32
+I32 = torch.int32
+TILE = 128
+
+
+def _draws(seed: int, n: int, k: int, forced_from: int | None = None) -> np.ndarray:
+    """k-means++ random stream of clustering.py:78-91 (numpy PCG64 default_rng):
+    ``rng.integers(n)`` then one ``rng.random()`` per step; steps from
+    ``forced_from`` on take ``rng.integers(n)`` (the ``total <= 0`` branch),
+    encoded as -(idx + 1)."""
+    rng = np.random.default_rng(seed)
+    out = np.empty(max(k, 1), np.float64)
+    out[0] = float(rng.integers(n))
+    for s in range(1, k):
+        if forced_from is not None and s >= forced_from:
+            out[s] = -(float(rng.integers(n)) + 1.0)
+        else:
+            out[s] = rng.random()
+    return out
+
+
+@dataclass
+class DevModel:
+    """Device-resident clustering result of one problem (views into a batch)."""
+    centers: torch.Tensor     # [k, D] f32
+    labels: torch.Tensor      # [n] int32
+    counts: torch.Tensor      # [k] int32
+    perm: torch.Tensor        # [n] int32 member order (stable argsort of labels)
+    starts: torch.Tensor      # [k+1] int32
+    status: torch.Tensor      # [8] int32
+    inertia: torch.Tensor     # [max_iter] f32
+    k: int
+    n: int
+    # multi-stage bookkeeping (host-known)
+    flag_full: bool = False
+    stage_count: int = 1
+    stage_mse: list = field(default_factory=list)
+    tau: float | None = None
+    host_iters: int | None = None   # when set, n_iter is host-known (multi-stage)
+
+    def n_iter(self) -> int:
+        if self.host_iters is not None:
+            return self.host_iters
+        return int(self.status[L.ST_NITER].item())
+
+
+class Batch:
+    """Flat device buffers + descriptor table for a batch of problems that
+    share D, dtype and the reference's GEMM accumulation order."""
+
+    def __init__(self, xs: list[torch.Tensor], ks: list[int], max_iter: int,
+                 kcaps: list[int] | None = None):
+        if not xs:
+            raise ParameterError("empty batch")
+        dev = L.device()
+        self.xs = xs
+        self.D = int(xs[0].shape[1])
+        self.dtype = L.dtype_code(xs[0])
+        self.P = len(xs)
+        self.ns = [int(x.shape[0]) for x in xs]
+        self.ks = [int(k) for k in ks]
+        self.kcaps = [int(c) for c in (kcaps or ks)]
+        self.max_iter = max(int(max_iter), 1)
+        self.orders = [L.gemm_order(n, k, self.D) for n, k in zip(self.ns, self.ks)]
+        if len(set(self.orders)) != 1:
+            raise ParameterError("batch mixes GEMM accumulation orders")
+        N, K, D, P = sum(self.ns), sum(self.kcaps), self.D, self.P
+        tiles = [(n + TILE - 1) // TILE for n in self.ns]
+        self.xx = torch.empty(N, dtype=F32, device=dev)
+        self.labels = torch.empty(N, dtype=I32, device=dev)
+        self.best = torch.empty(N, dtype=F32, device=dev)
+        self.perm = torch.empty(N, dtype=I32, device=dev)
+        self.dscratch = torch.empty(N, dtype=torch.float64, device=dev)
+        self.centers = torch.empty(K * D, dtype=F32, device=dev)
+        self.cc = torch.empty(K, dtype=F32, device=dev)
+        self.counts = torch.empty(K, dtype=I32, device=dev)
+        self.starts = torch.empty(K + P, dtype=I32, device=dev)
+        self.movement = torch.empty(K, dtype=F32, device=dev)
+        self.tile_hist = torch.empty(max(sum(t * c for t, c in zip(tiles, self.kcaps)), 1),
+                                     dtype=I32, device=dev)
+        self.inertia = torch.zeros(P * self.max_iter, dtype=F32, device=dev)
+        self.status = torch.zeros(P * L.STATUS_WORDS, dtype=I32, device=dev)
+        desc = np.zeros(P, dtype=L.PROBLEM_DTYPE)
+        self.n_off, self.k_off, self.t_off = [], [], []
+        no = ko = to = 0
+        for p in range(P):
+            x = xs[p]
+            if not x.is_contiguous() or x.shape[1] != D or x.dtype != xs[0].dtype:
+                raise DimensionError("batch inputs must be contiguous [n, D] of one dtype")
+            self.n_off.append(no)
+            self.k_off.append(ko)
+            self.t_off.append(to)
+            e = desc[p]
+            e["x"] = x.data_ptr()
+            e["xx"] = self.xx.data_ptr() + 4 * no
+            e["centers"] = self.centers.data_ptr() + 4 * ko * D
+            e["cc"] = self.cc.data_ptr() + 4 * ko
+            e["labels"] = self.labels.data_ptr() + 4 * no
+            e["best"] = self.best.data_ptr() + 4 * no
+            e["counts"] = self.counts.data_ptr() + 4 * ko
+            e["perm"] = self.perm.data_ptr() + 4 * no
+            e["starts"] = self.starts.data_ptr() + 4 * (ko + p)
+            e["tile_hist"] = self.tile_hist.data_ptr() + 4 * to
+            e["inertia"] = self.inertia.data_ptr() + 4 * p * self.max_iter
+            e["movement"] = self.movement.data_ptr() + 4 * ko
+            e["status"] = self.status.data_ptr() + 4 * p * L.STATUS_WORDS
+            e["plan_n"] = L.pw_plan(self.ns[p]).data_ptr()
+            e["plan_k"] = 0
+            e["dscratch"] = self.dscratch.data_ptr() + 8 * no
+            e["n"] = self.ns[p]
+            e["k"] = self.ks[p]
+            e["order"] = self.orders[p]
+            no += self.ns[p]
+            ko += self.kcaps[p]
+            to += tiles[p] * self.kcaps[p]
+        self.desc = desc
+        self.dev = L.to_device_struct(desc)
+        self.max_n = max(self.ns)
+        self.max_k = max(self.kcaps)
+
+    # views -------------------------------------------------------------
+    def centers_of(self, p: int, k: int | None = None) -> torch.Tensor:
+        k = self.ks[p] if k is None else k
+        o = self.k_off[p] * self.D
+        return self.centers[o:o + k * self.D].view(k, self.D)
+
+    def model(self, p: int) -> DevModel:
+        n, k, no, ko = self.ns[p], self.ks[p], self.n_off[p], self.k_off[p]
+        return DevModel(
+            centers=self.centers_of(p), labels=self.labels[no:no + n],
+            counts=self.counts[ko:ko + k], perm=self.perm[no:no + n],
+            starts=self.starts[ko + p:ko + p + k + 1],
+            status=self.status[p * L.STATUS_WORDS:(p + 1) * L.STATUS_WORDS],
+            inertia=self.inertia[p * self.max_iter:(p + 1) * self.max_iter], k=k, n=n)
+
+    def best_of(self, p: int) -> torch.Tensor:
+        return self.best[self.n_off[p]:self.n_off[p] + self.ns[p]]
+
+    # kernels -------------------------------------------------------------
+    def args(self):
+        return (self.dev.data_ptr(), self.P, self.dtype, self.D, self.max_n, self.max_k)
+
+    def kmeanspp(self, draws: torch.Tensor, max_k: int):
+        L.call("ac_kmeanspp", self.dev.data_ptr(), self.P, self.dtype, self.D, self.max_n, max_k,
+               draws.data_ptr(), L.stream_ptr())
+
+    def lloyd(self, max_iter: int, tol: float, poll_every: int = 0):
+        L.call("ac_lloyd", *self.args(), int(max_iter), float(tol), int(poll_every),
+               self.desc.ctypes.data, L.stream_ptr())
+
+    def prepare(self):
+        L.call("ac_lloyd_prepare", *self.args(), L.stream_ptr())
+
+    def assign(self, c_lo: int = 0, flags: int = L.ASSIGN_ALL):
+        L.call("ac_assign_ordered", *self.args(), int(c_lo), int(flags), self.orders[0],
+               L.stream_ptr())
+
+    def sort(self):
+        """tile histograms must be current (written by assign)."""
+        L.call("ac_repair_sort", *self.args(), -1, L.ASSIGN_ALL, L.stream_ptr())
+
+
+def _group_by_order(ns, ks, D):
+    groups: dict[int, list[int]] = {}
+    for i, (n, k) in enumerate(zip(ns, ks)):
+        groups.setdefault(L.gemm_order(n, k, D), []).append(i)
+    return list(groups.values())
+
+
+# ---------------------------------------------------------------------------
+# k-means / Lloyd
+# ---------------------------------------------------------------------------
+def kmeans_batch(xs: list[torch.Tensor], ks: list[int], seeds: list[int], max_iter: int,
+                 tol: float) -> list[DevModel]:
+    """clustering.py:155-167 for every problem (k-means++ then Lloyd)."""
+    out: list[DevModel | None] = [None] * len(xs)
+    D = int(xs[0].shape[1])
+    for idx in _group_by_order([x.shape[0] for x in xs], ks, D):
+        sub_x = [xs[i] for i in idx]
+        sub_k = [ks[i] for i in idx]
+        sub_s = [seeds[i] for i in idx]
+        b = Batch(sub_x, sub_k, max_iter)
+        mk = max(sub_k)
+        draws = np.zeros((len(idx), mk), np.float64)
+        for j, (x, k, s) in enumerate(zip(sub_x, sub_k, sub_s)):
+            draws[j, :k] = _draws(s, int(x.shape[0]), k)
+        dd = torch.from_numpy(draws).to(L.device(), non_blocking=True)
+        b.kmeanspp(dd, mk)
+        # k-means++ `total <= 0` replay (all remaining points coincide with a
+        # chosen centre): rare; requires a host look at the stop flags
+        stops = b.status.view(b.P, L.STATUS_WORDS)[:, L.ST_KPP_STOP].cpu().numpy()
+        if (stops >= 0).any():
+            for j in np.flatnonzero(stops >= 0):
+                draws[j, :sub_k[j]] = _draws(sub_s[j], int(sub_x[j].shape[0]), sub_k[j],
+                                             forced_from=int(stops[j]))
+            dd = torch.from_numpy(draws).to(L.device())
+            b.kmeanspp(dd, mk)
+        b.lloyd(max_iter, tol)
+        for j, i in enumerate(idx):
+            out[i] = b.model(j)
+    return out  # type: ignore[return-value]
+
+
+def lloyd_batch(xs: list[torch.Tensor], inits: list[torch.Tensor], max_iter: int,
+                tol: float) -> list[DevModel]:
+    """clustering.py:119-152 from given initial centres (warm starts)."""
+    out: list[DevModel | None] = [None] * len(xs)
+    D = int(xs[0].shape[1])
+    ks = [int(c.shape[0]) for c in inits]
+    for idx in _group_by_order([x.shape[0] for x in xs], ks, D):
+        b = Batch([xs[i] for i in idx], [ks[i] for i in idx], max_iter)
+        for j, i in enumerate(idx):
+            b.centers_of(j).copy_(inits[i].to(F32))
+        b.lloyd(max_iter, tol)
+        for j, i in enumerate(idx):
+            out[i] = b.model(j)
+    return out  # type: ignore[return-value]
+
+
+def l2norm(x: torch.Tensor):
+    """tensorops.py:59-76 on device: (rows f32, degenerate mask u8)."""
+    rows, d = x.shape
+    out = torch.empty((rows, d), dtype=F32, device=x.device)
+    deg = torch.empty(rows, dtype=torch.uint8, device=x.device)
+    L.call("ac_l2norm", x.data_ptr(), L.dtype_code(x), rows, d, out.data_ptr(), 0,
+           deg.data_ptr(), L.stream_ptr())
+    return out, deg
+
+
+def segment_means(xs: list[torch.Tensor], models: list[DevModel]) -> list[torch.Tensor]:
+    """f64 member means in member order (cluster_queries reps, clustering.py:197-200)."""
+    outs = [torch.empty((m.k, x.shape[1]), dtype=F32, device=x.device) for x, m in zip(xs, models)]
+    # a minimal descriptor table pointing at the models' buffers
+    desc = np.zeros(len(xs), dtype=L.PROBLEM_DTYPE)
+    for p, (x, m) in enumerate(zip(xs, models)):
+        e = desc[p]
+        e["x"] = x.data_ptr()
+        e["counts"] = m.counts.data_ptr()
+        e["perm"] = m.perm.data_ptr()
+        e["starts"] = m.starts.data_ptr()
+        e["n"] = m.n
+        e["k"] = m.k
+    dv = L.to_device_struct(desc)
+    ptrs = torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64).to(L.device())
+    L.call("ac_segment_mean", dv.data_ptr(), len(xs), L.dtype_code(xs[0]), int(xs[0].shape[1]),
+           max(m.k for m in models), ptrs.data_ptr(), L.stream_ptr())
+    return outs
+
+
+def cluster_queries_batch(qs: list[torch.Tensor], num_clusters: list[int], seeds: list[int],
+                          max_iter: int, tol: float, inits: list[torch.Tensor] | None = None):
+    """clustering.py:182-200: normalise, cluster (cold or warm), representatives."""
+    qns = [l2norm(q)[0] for q in qs]
+    if inits is None:
+        models = kmeans_batch(qns, num_clusters, seeds, max_iter, tol)
+    else:
+        models = lloyd_batch(qns, inits, max_iter, tol)
+    reps = segment_means(qns, models)
+    return models, reps, qns
+
+
+# ---------------------------------------------------------------------------
+# tau / mse / multi-stage
+# ---------------------------------------------------------------------------
+def _model_desc(xs: list[torch.Tensor], models: list[DevModel], scratch: list[torch.Tensor]):
+    desc = np.zeros(len(xs), dtype=L.PROBLEM_DTYPE)
+    for p, (x, m, s) in enumerate(zip(xs, models, scratch)):
+        e = desc[p]
+        e["x"] = x.data_ptr()
+        e["centers"] = m.centers.data_ptr()
+        e["labels"] = m.labels.data_ptr()
+        e["plan_n"] = L.pw_plan(m.n).data_ptr()
+        e["dscratch"] = s.data_ptr()
+        e["n"] = m.n
+        e["k"] = m.k
+    return L.to_device_struct(desc)
+
+
+def tau_batch(ks: list[torch.Tensor], stage0: list[DevModel], factor: float) -> torch.Tensor:
+    """compute_tau (clustering.py:209-215) for every problem -> f64 [P] device."""
+    scratch = [torch.empty(m.n, dtype=torch.float64, device=L.device()) for m in stage0]
+    dv = _model_desc(ks, stage0, scratch)
+    out = torch.empty(len(ks), dtype=torch.float64, device=L.device())
+    L.call("ac_tau", dv.data_ptr(), len(ks), L.dtype_code(ks[0]), int(ks[0].shape[1]),
+           max(m.n for m in stage0), float(factor), out.data_ptr(), L.stream_ptr())
+    return out
+
+
+def mse_batch(ks: list[torch.Tensor], models: list[DevModel]) -> torch.Tensor:
+    """pipeline.py:319-323 per-head clustering MSE (f64) -> [P] device."""
+    scratch = [torch.empty(m.n, dtype=torch.float64, device=L.device()) for m in models]
+    dv = _model_desc(ks, models, scratch)
+    out = torch.empty(len(ks), dtype=torch.float64, device=L.device())
+    L.call("ac_mse_f64", dv.data_ptr(), len(ks), L.dtype_code(ks[0]), int(ks[0].shape[1]),
+           max(m.n for m in models), out.data_ptr(), L.stream_ptr())
+    return out
+
+
+class _RunningAssign:
+    """nearest-centre state of all N keys against the accumulated multi-stage
+    centres: running (best, label) merged round by round with strict '<'
+    (earlier centres win ties, exactly like argmin over the concatenation)."""
+
+    def __init__(self, k: torch.Tensor, kcap: int, max_iter: int):
+        self.k = k
+        self.batch = Batch([k], [1], max_iter, kcaps=[kcap])
+        self.batch.prepare()  # ||x||^2 of every key (the centres are set per round)
+        self.nc = 0
+        self.orders: list[int] = []
+
+    def add(self, centers: torch.Tensor):
+        b = self.batch
+        m = centers.shape[0]
+        b.centers_of(0, self.nc + m)[self.nc:].copy_(centers)
+        new_nc = self.nc + m
+        order = L.gemm_order(b.ns[0], new_nc, b.D)
+        full = not self.orders or any(o != order for o in self.orders) or self.nc == 0
+        b.desc[0]["k"] = new_nc
+        b.desc[0]["order"] = order
+        b.orders = [order]
+        b.ks = [new_nc]
+        b.dev = L.to_device_struct(b.desc)
+        if full:
+            b.assign(0, L.ASSIGN_ALL)
+        else:
+            b.assign(self.nc, L.ASSIGN_ALL | L.ASSIGN_MERGE)
+        self.orders.append(order)
+        self.nc = new_nc
+
+    def mean_best(self) -> torch.Tensor:
+        b = self.batch
+        out = torch.empty(1, dtype=F32, device=L.device())
+        L.call("ac_reduce_best", b.dev.data_ptr(), 1, b.max_n, 0, out.data_ptr(), L.stream_ptr())
+        return out
+
+
+def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0: int,
+                      seeds: list[int], max_iter: int, tol: float,
+                      stage0: list[DevModel | None], schedule=None) -> list[DevModel]:
+    """multi_stage_cluster_keys (clustering.py:218-320, default schedule) for
+    several keys tensors in lock-step rounds.  Rounds need |U| on the host."""
+    dev = L.device()
+    H = len(ks)
+    D = int(ks[0].shape[1])
+    dt = L.dtype_code(ks[0])
+    results: list[DevModel | None] = [None] * H
+    st = []
+    for h in range(H):
+        n = int(ks[h].shape[0])
+        st.append(dict(n=n, pool=torch.arange(n, dtype=torch.int64, device=dev), size=n,
+                       nc=0, rnd=0, flag=False, iters=0, mse=[], blocks=[],
+                       run=_RunningAssign(ks[h], n_max + m0, max_iter)))
+    live = [h for h in range(H) if taus[h] > 0.0]
+    for h in range(H):
+        if taus[h] <= 0.0:
+            base = stage0[h] if stage0[h] is not None else kmeans_batch(
+                [ks[h]], [min(m0, st[h]["n"])], [seeds[h]], max_iter, tol)[0]
+            ra = st[h]["run"]
+            ra.add(base.centers)
+            base.flag_full = True
+            base.stage_count = 1
+            base.stage_mse = [float(ra.mean_best().item())]
+            base.tau = float(taus[h])
+            base.host_iters = base.n_iter()
+            results[h] = base
+    while live:
+        todo = []
+        for h in live:
+            s = st[h]
+            if s["nc"] >= n_max:
+                s["flag"] = True
+                continue
+            if schedule is not None:
+                want = int(schedule(s["rnd"], s["size"], s["n"]))
+            else:
+                want = m0 if s["rnd"] == 0 else max(8, math.ceil(m0 * s["size"] / s["n"]))
+            s["m_t"] = min(want, s["size"])
+            todo.append(h)
+        if not todo:
+            break
+        # this round's clustering (stage 0 reused for round 0)
+        need, subx = [], {}
+        for h in todo:
+            s = st[h]
+            if s["rnd"] == 0 and stage0[h] is not None and stage0[h].k == s["m_t"]:
+                s["model"], s["sub"] = stage0[h], ks[h]
+            else:
+                if s["size"] == s["n"]:
+                    sub = ks[h]
+                else:
+                    sub = torch.empty((s["size"], D), dtype=ks[h].dtype, device=dev)
+                    L.call("ac_gather_rows", ks[h].data_ptr(), dt, D, s["pool"].data_ptr(),
+                           s["size"], sub.data_ptr(), L.stream_ptr())
+                subx[h] = sub
+                need.append(h)
+        if need:
+            ms = kmeans_batch([subx[h] for h in need], [st[h]["m_t"] for h in need],
+                              [seeds[h] + st[h]["rnd"] for h in need], max_iter, tol)
+            for h, m in zip(need, ms):
+                st[h]["model"], st[h]["sub"] = m, subx[h]
+        # retire: U = U[dist >= tau] (f32 compare, NEP 50)
+        desc = np.zeros(len(todo), dtype=L.PROBLEM_DTYPE)
+        outs, scratch = [], []
+        for j, h in enumerate(todo):
+            s = st[h]
+            m = s["model"]
+            sc = torch.empty(s["size"], dtype=torch.float64, device=dev)
+            scratch.append(sc)
+            e = desc[j]
+            e["x"] = s["sub"].data_ptr()
+            e["centers"] = m.centers.data_ptr()
+            e["labels"] = m.labels.data_ptr()
+            e["dscratch"] = sc.data_ptr()
+            e["n"] = s["size"]
+            e["k"] = m.k
+            outs.append(torch.empty(s["size"], dtype=torch.int64, device=dev))
+        dv = L.to_device_struct(desc)
+        tau32 = torch.tensor([np.float32(taus[h]) for h in todo], dtype=F32).to(dev)
+        pin = torch.tensor([st[h]["pool"].data_ptr() for h in todo], dtype=torch.int64).to(dev)
+        pout = torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64).to(dev)
+        cnt = torch.empty(len(todo), dtype=torch.int64, device=dev)
+        L.call("ac_retire", dv.data_ptr(), len(todo), dt, D, max(st[h]["size"] for h in todo),
+               tau32.data_ptr(), pin.data_ptr(), pout.data_ptr(), cnt.data_ptr(), L.stream_ptr())
+        mses = []
+        for h in todo:
+            s = st[h]
+            s["iters"] += s["model"].n_iter()
+            s["run"].add(s["model"].centers)
+            s["blocks"].append(s["model"].k)
+            s["nc"] += s["model"].k
+            mses.append(s["run"].mean_best())
+        cnt_h = cnt.cpu().numpy()
+        mse_h = torch.cat(mses).cpu().numpy()
+        for j, h in enumerate(todo):
+            s = st[h]
+            s["pool"] = outs[j][:int(cnt_h[j])]
+            s["size"] = int(cnt_h[j])
+            s["mse"].append(float(mse_h[j]))
+            s["rnd"] += 1
+        live = [h for h in live if st[h]["size"] > 0 and not st[h]["flag"]]
+        for h in list(live):
+            if st[h]["nc"] >= n_max:
+                st[h]["flag"] = True
+                live.remove(h)
+    # final labels = running argmin over every accumulated centre; drop empties
+    fin = [h for h in range(H) if results[h] is None]
+    for h in fin:
+        s = st[h]
+        b = s["run"].batch
+        newk = torch.empty(1, dtype=I32, device=dev)
+        L.call("ac_drop_empty", b.dev.data_ptr(), 1, D, b.max_n, b.max_k, newk.data_ptr(),
+               L.stream_ptr())
+        kk = int(newk.item())
+        b.desc[0]["k"] = kk
+        b.ks = [kk]
+        b.dev = L.to_device_struct(b.desc)
+        L.call("ac_sort_by_label", b.dev.data_ptr(), 1, b.max_n, b.max_k, L.stream_ptr())
+        m = b.model(0)
+        m.flag_full = s["flag"]
+        m.stage_count = s["rnd"]
+        m.stage_mse = s["mse"]
+        m.tau = float(taus[h])
+        m.host_iters = s["iters"]
+        results[h] = m
+    return results  # type: ignore[return-value]
+
+
+# ---------------------------------------------------------------------------
+# selection + attention
+# ---------------------------------------------------------------------------
+def envelopes_batch(ks: list[torch.Tensor], models: list[DevModel]):
+    D = int(ks[0].shape[1])
+    emax = [torch.empty((m.k, D), dtype=F32, device=L.device()) for m in models]
+    emin = [torch.empty((m.k, D), dtype=F32, device=L.device()) for m in models]
+    desc = np.zeros(len(ks), dtype=L.PROBLEM_DTYPE)
+    for p, (x, m) in enumerate(zip(ks, models)):
+        e = desc[p]
+        e["x"] = x.data_ptr()
+        e["counts"] = m.counts.data_ptr()
+        e["perm"] = m.perm.data_ptr()
+        e["starts"] = m.starts.data_ptr()
+        e["n"] = m.n
+        e["k"] = m.k
+    dv = L.to_device_struct(desc)
+    pmax = torch.tensor([t.data_ptr() for t in emax], dtype=torch.int64).to(L.device())
+    pmin = torch.tensor([t.data_ptr() for t in emin], dtype=torch.int64).to(L.device())
+    L.call("ac_envelopes", dv.data_ptr(), len(ks), L.dtype_code(ks[0]), D,
+           max(m.k for m in models), pmax.data_ptr(), pmin.data_ptr(), L.stream_ptr())
+    return emax, emin
+
+
+@dataclass
+class DevSelection:
+    scores: torch.Tensor     # [gq, C] f32
+    selected: torch.Tensor   # [gq, topk] int64
+    runs: torch.Tensor       # [gq, run_stride, 2] int32
+    nruns: torch.Tensor      # [gq] int32
+    density: torch.Tensor    # [1] f64
+
+
+def select_batch(reps: list[torch.Tensor], emax: list[torch.Tensor], emin: list[torch.Tensor],
+                 kmodels: list[DevModel], topks: list[int], scorer: str,
+                 run_stride: int | None = None, scores_in: list[torch.Tensor] | None = None):
+    """quest.py:94-143: scores, stable top-k, merged runs, density."""
+    dev = L.device()
+    P = len(reps)
+    D = int(reps[0].shape[1])
+    stride = run_stride or max(topks)
+    out = []
+    desc = np.zeros(P, dtype=L.SELECT_DTYPE)
+    gq_max = max(int(r.shape[0]) for r in reps)
+    runs = torch.zeros((P, gq_max, stride, 2), dtype=I32, device=dev)
+    nruns = torch.zeros((P, gq_max), dtype=I32, device=dev)
+    for p in range(P):
+        gq, C = int(reps[p].shape[0]), kmodels[p].k
+        sel = DevSelection(
+            scores=(scores_in[p] if scores_in is not None
+                    else torch.empty((gq, C), dtype=F32, device=dev)),
+            selected=torch.empty((gq, topks[p]), dtype=torch.int64, device=dev),
+            runs=runs[p], nruns=nruns[p],
+            density=torch.empty(1, dtype=torch.float64, device=dev))
+        cov = torch.empty(gq, dtype=torch.int64, device=dev)
+        sel._covered = cov  # keep alive
+        e = desc[p]
+        e["reps"] = reps[p].data_ptr()
+        e["emax"] = emax[p].data_ptr()
+        e["emin"] = emin[p].data_ptr()
+        e["counts"] = kmodels[p].counts.data_ptr()
+        e["kstarts"] = kmodels[p].starts.data_ptr()
+        e["scores"] = sel.scores.data_ptr()
+        e["selected"] = sel.selected.data_ptr()
+        e["runs"] = sel.runs.data_ptr()
+        e["nruns"] = sel.nruns.data_ptr()
+        e["covered"] = cov.data_ptr()
+        e["density"] = sel.density.data_ptr()
+        e["gq"], e["c"], e["topk"] = gq, C, topks[p]
+        e["order"] = L.gemm_order(gq, C, D)
+        e["run_stride"] = stride
+        out.append(sel)
+    dv = L.to_device_struct(desc)
+    L.call("ac_select", dv.data_ptr(), P, D, L.SCORERS[scorer], gq_max,
+           max(m.k for m in kmodels), stride, L.stream_ptr())
+    return out, runs, nruns
+
+
+ATTN_DIMS = (16, 32, 64, 128)
+
+
+def _attn_dim(d: int) -> int:
+    for a in ATTN_DIMS:
+        if d <= a:
+            return a
+    raise DimensionError(f"head_dim {d} > 128 is not supported by the attention kernel")
+
+
+def _pad_dim(x: torch.Tensor, da: int) -> torch.Tensor:
+    if x.shape[-1] == da:
+        return x.contiguous()
+    return torch.nn.functional.pad(x, (0, da - x.shape[-1])).contiguous()
+
+
+def sparse_attention_heads(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                           qmodels: list[DevModel], kmodels: list[DevModel],
+                           runs: torch.Tensor, nruns: torch.Tensor, out_dtype=F32,
+                           impl: str = "auto") -> torch.Tensor:
+    """_gathered_attention (pipeline.py:154-165) for H heads of one layer.
+    q/k/v: [H, L, D] (f32 or bf16).  Returns [H, L, D] out_dtype."""
+    H, Ln, D = q.shape
+    dev = L.device()
+    da = _attn_dim(D)
+    dt = L.dtype_code(q)
+    qa, ka, va = (_pad_dim(t, da) for t in (q, k, v))
+    kp = torch.empty_like(ka)
+    vp = torch.empty_like(va)
+    kperm = torch.stack([m.perm for m in kmodels])
+    L.call("ac_permute_rows_heads", ka.data_ptr(), dt, da, kperm.data_ptr(), Ln, H, kp.data_ptr(),
+           L.stream_ptr())
+    L.call("ac_permute_rows_heads", va.data_ptr(), dt, da, kperm.data_ptr(), Ln, H, vp.data_ptr(),
+           L.stream_ptr())
+    gq = torch.tensor([m.k for m in qmodels], dtype=I32).to(dev)
+    gq_max = int(runs.shape[1])
+    topk_max = int(runs.shape[2])
+    qperm = torch.stack([m.perm for m in qmodels])
+    qlab = torch.stack([m.labels for m in qmodels])
+    qcounts = torch.zeros((H, gq_max), dtype=I32, device=dev)
+    qstarts = torch.zeros((H, gq_max + 1), dtype=I32, device=dev)
+    for h, m in enumerate(qmodels):
+        qcounts[h, :m.k] = m.counts
+        qstarts[h, :m.k + 1] = m.starts
+    qp_cap = Ln + TILE * gq_max
+    item_cap = (Ln + TILE - 1) // TILE + gq_max
+    qp = torch.empty((H * qp_cap, da), dtype=q.dtype, device=dev)
+    qidx = torch.empty(H * qp_cap + H * gq_max, dtype=I32, device=dev)
+    items = torch.empty(H * item_cap * L.ITEM_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    L.call("ac_build_q_layout", qa.data_ptr(), dt, da, Ln, H, qperm.data_ptr(), qstarts.data_ptr(),
+           qcounts.data_ptr(), qlab.data_ptr(), gq.data_ptr(), gq_max, nruns.data_ptr(), topk_max,
+           qp.data_ptr(), qidx.data_ptr(), qp_cap, items.data_ptr(), item_cap, L.stream_ptr())
+    out = torch.empty((H, Ln, da), dtype=out_dtype, device=dev)
+    fn = "ac_sparse_attention" if impl == "auto" else "ac_sparse_attention_simt"
+    L.call(fn, qp.data_ptr(), qidx.data_ptr(), kp.data_ptr(), vp.data_ptr(), dt, da, Ln,
+           items.data_ptr(), H * item_cap, runs.data_ptr(), float(1.0 / math.sqrt(D)),
+           out.data_ptr(), L.dtype_code(out) if out_dtype != F32 else L.DTYPE_F32, L.stream_ptr())
+    return out[..., :D] if da != D else out
+
+
+def dense_attention_heads(q, k, v, out_dtype=F32, impl: str = "auto") -> torch.Tensor:
+    """full_attention (reference.py:25-45) for H heads: one run covering all keys."""
+    H, Ln, D = q.shape
+    dev = L.device()
+    qm = []
+    km = []
+    ar = torch.arange(Ln, dtype=I32, device=dev)
+    for _ in range(H):
+        qm.append(DevModel(centers=None, labels=torch.zeros(Ln, dtype=I32, device=dev),
+                           counts=torch.tensor([Ln], dtype=I32, device=dev), perm=ar,
+                           starts=torch.tensor([0, Ln], dtype=I32, device=dev), status=None,
+                           inertia=None, k=1, n=Ln))
+        km.append(DevModel(centers=None, labels=None, counts=None, perm=ar, starts=None,
+                           status=None, inertia=None, k=1, n=Ln))
+    runs = torch.zeros((H, 1, 1, 2), dtype=I32, device=dev)
+    runs[..., 1] = Ln
+    nruns = torch.ones((H, 1), dtype=I32, device=dev)
+    return sparse_attention_heads(q, k, v, qm, km, runs, nruns, out_dtype, impl)

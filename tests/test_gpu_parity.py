@@ -1,0 +1,224 @@
+"""CUDA path vs the bit-exact CPU oracle on identical seeded inputs.
+
+Integer/label/selection results must be bit-identical; clustering floats
+(centres, inertia, tau, stage MSE) too, because the oracle restates the
+reference arithmetic exactly.  Attention outputs: rel-L2 <= 1e-4 for f32
+inputs, <= 1e-2 for bf16 inputs (BASELINE.json north_star tolerances).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2604_18348_b200.synthetic import CRIT7_SPEC, LayerSpec, gen_synthetic
+
+pytestmark = pytest.mark.gpu
+
+F32_TOL = 1e-4
+BF16_TOL = 1e-2
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(a), 1e-30))
+
+
+def same_model(dev, ora, inertia=True):
+    assert np.array_equal(dev.assignments, ora.assignments)
+    assert np.array_equal(dev.centers, ora.centers)
+    assert np.array_equal(np.asarray(dev.counts, np.int64), np.asarray(ora.counts, np.int64))
+    assert dev.n_iter == ora.n_iter
+    if inertia:
+        assert list(dev.inertia_history) == list(ora.inertia_history)
+
+
+def bf16_round(a):
+    return torch.from_numpy(a).bfloat16().float().numpy()
+
+
+@pytest.mark.parametrize("n,d,k,seed", [
+    (6, 3, 6, 1), (12, 2, 2, 2), (20, 4, 1, 0), (40, 2, 15, 0), (60, 6, 5, 3),
+    (200, 8, 10, 4), (300, 64, 8, 2), (500, 32, 16, 1), (1000, 64, 20, 3),
+    (2000, 16, 50, 5), (4096, 64, 65, 0), (3000, 128, 100, 7), (700, 17, 9, 11),
+])
+def test_kmeans_bit_exact(gpu, oracle, n, d, k, seed):
+    rng = np.random.default_rng(seed + 100)
+    x = (rng.normal(size=(n, d)) * 3).astype(np.float32)
+    a = gpu.kmeans(x, k, seed=seed)
+    b = oracle.kmeans(x, k, seed)
+    same_model(a, b, inertia=k > 1)
+
+
+def test_l2norm_bit_exact(gpu, oracle):
+    rng = np.random.default_rng(0)
+    x = (rng.normal(size=(777, 64)) * rng.lognormal(size=(777, 1))).astype(np.float32)
+    x[3] = 0
+    x[5] = x[5] / np.linalg.norm(x[5])
+    nr = gpu.l2_normalize_rows(x)
+    ro, deg = oracle.l2_normalize(x)
+    assert np.array_equal(nr.rows, ro)
+    assert list(nr.degenerate) == list(deg) == [3]
+
+
+@pytest.mark.parametrize("L,D,dtype", [(2048, 64, "f32"), (4096, 64, "bf16"), (3000, 128, "bf16")])
+def test_plan_pieces_bit_exact(gpu, oracle, L, D, dtype):
+    q, k, v = gen_synthetic(CRIT7_SPEC, L, D, 1, 1, 0)[0][0]
+    if dtype == "bf16":
+        q, k = bf16_round(q), bf16_round(k)
+        kt = torch.from_numpy(k).bfloat16().cuda()
+    else:
+        kt = k
+    qa, ra = gpu.cluster_queries(q, 65, 0)
+    qb, rb = oracle.cluster_queries(q, 65, 0)
+    same_model(qa, qb)
+    assert np.array_equal(ra, rb)
+    s0a = gpu.kmeans(kt, 100, 0)
+    s0b = oracle.kmeans(k, 100, 0)
+    same_model(_host(s0a), s0b)
+    ta = gpu.compute_tau(k, s0b)
+    tb = oracle.compute_tau(k, s0b)
+    assert ta == tb
+    ma = gpu.multi_stage_cluster_keys(k, tb, stage0=s0b)
+    mb = oracle.multi_stage(k, tb, stage0=s0b)
+    assert np.array_equal(ma.assignments, mb.assignments)
+    assert np.array_equal(ma.centers, mb.centers)
+    assert ma.stage_mse == mb.stage_mse and ma.stage_count == mb.stage_count
+    assert ma.n_iter == mb.n_iter and ma.flag_full == mb.flag_full
+
+
+def _host(m):
+    import dataclasses
+    out = dataclasses.replace(m)
+    for f in ("centers", "assignments", "counts"):
+        v = getattr(m, f)
+        if isinstance(v, torch.Tensor):
+            setattr(out, f, v.cpu().numpy())
+    return out
+
+
+@pytest.mark.parametrize("kind,L,D,m0,nmax", [
+    ("mixed", 1024, 16, 16, 200), ("compact", 512, 8, 16, 1000), ("dispersed", 512, 8, 16, 64),
+    ("mixed", 2048, 64, 32, 1000),
+])
+def test_multi_stage_rounds_bit_exact(gpu, oracle, kind, L, D, m0, nmax):
+    spec = LayerSpec(kind=kind, gaussian_components=8, component_sigma=0.5,
+                     component_separation=20.0)
+    q, k, v = gen_synthetic(spec, L, D, 1, 1, 3)[0][0]
+    s0 = oracle.kmeans(k, m0, 1)
+    tau = oracle.compute_tau(k, s0)
+    ma = gpu.multi_stage_cluster_keys(k, tau, n_max=nmax, m0=m0, seed=1, stage0=s0)
+    mb = oracle.multi_stage(k, tau, n_max=nmax, m0=m0, seed=1, stage0=s0)
+    assert ma.stage_count == mb.stage_count
+    assert ma.flag_full == mb.flag_full
+    assert np.array_equal(ma.assignments, mb.assignments)
+    assert np.array_equal(ma.centers, mb.centers)
+    assert ma.stage_mse == mb.stage_mse
+    assert ma.n_iter == mb.n_iter
+
+
+@pytest.mark.parametrize("gq,c,d", [(2, 3, 4), (8, 16, 32), (5, 7, 11), (65, 100, 64),
+                                    (30, 30, 64), (7, 9, 32), (65, 17, 64), (3, 40, 48)])
+def test_selection_bit_exact(gpu, oracle, gq, c, d):
+    rng = np.random.default_rng(gq * 100 + c)
+    x = rng.normal(size=(c * 4, d)).astype(np.float32)
+    m = oracle.kmeans(x, c, 0)
+    env_o = oracle.envelopes(x, m)
+    env_g = gpu.build_envelopes(x, m)
+    assert np.array_equal(env_g.max_vec, env_o.max_vec)
+    assert np.array_equal(env_g.min_vec, env_o.min_vec)
+    assert np.array_equal(env_g.member_order, env_o.member_order)
+    assert np.array_equal(env_g.member_starts, env_o.member_starts)
+    reps = rng.normal(size=(gq, d)).astype(np.float32)
+    s_g = gpu.tensor_quest(reps, env_g)
+    s_o = oracle.scores(reps, env_o.max_vec, env_o.min_vec, "quest")
+    assert np.array_equal(s_g, s_o)
+    assert np.array_equal(gpu.mean_center_scores(reps, m.centers),
+                          oracle.scores(reps, m.centers, m.centers, "mean"))
+    assert np.array_equal(gpu.tensor_quest_clamped_centers(reps, m.centers),
+                          oracle.scores(reps, m.centers, m.centers, "clamped"))
+    for topk in (1, min(3, c), c):
+        a = gpu.select_topk_clusters(s_o, topk, m.counts)
+        b = oracle.select_topk(s_o, topk, m.counts)
+        assert np.array_equal(a.selected, b.selected)
+        assert a.density == b.density
+
+
+def test_selection_ties_lower_index(gpu):
+    s = np.array([[1.0, 2.0, 2.0], [3.0, 1.0, 2.0]], np.float32)
+    r = gpu.select_topk_clusters(s, 2, np.array([1, 1, 1]))
+    assert r.selected.tolist() == [[1, 2], [0, 2]]
+
+
+@pytest.mark.parametrize("L,D", [(300, 16), (1000, 64), (517, 32), (256, 128)])
+def test_full_attention_f32(gpu, oracle, L, D):
+    rng = np.random.default_rng(L)
+    q, k, v = (rng.normal(size=(L, D)).astype(np.float32) for _ in range(3))
+    a = gpu.full_attention(q, k, v)
+    b = oracle.full_attention(q, k, v)
+    assert rel_l2(b, a) <= F32_TOL
+
+
+def test_head_c1_f32_sparse(gpu, oracle):
+    """C1-shaped head (L=4096, D=64, f32), crit-7 spec, topk 25."""
+    q, k, v = gen_synthetic(CRIT7_SPEC, 4096, 64, 1, 1, 0)[0][0]
+    p = gpu.PipelineParams(q_clusters=65, topk=25, full_layer_quota=0.0)
+    op = oracle.Params(q_clusters=65, topk=25, full_layer_quota=0.0)
+    out, hs = gpu.adacluster_attention(q, k, v, gpu.LayerPolicy(topk=25), gpu.StepState(), 0, p)
+    r = oracle.head_step(q, k, v, None, oracle.HeadState(), 0, op)
+    assert hs.mode == r.mode == "sparse"
+    assert np.array_equal(hs.q_model.assignments, r.q_model.assignments)
+    assert np.array_equal(hs.key_model.assignments, r.key_model.assignments)
+    assert np.array_equal(hs.selection.selected, r.selection.selected)
+    assert hs.density == r.selection.density
+    assert hs.key_iters == r.key_iters and hs.query_iters == r.query_iters
+    assert rel_l2(r.out, out) <= F32_TOL
+
+
+def test_head_bf16_sparse(gpu, oracle):
+    """bf16 inputs (C2-like spec, smaller L): clustering bit-exact on the
+    upcast values, output within 1e-2 of the oracle's f32 sparse output."""
+    q, k, v = gen_synthetic(CRIT7_SPEC, 8192, 64, 1, 1, 0)[0][0]
+    qb, kb, vb = (torch.from_numpy(a).bfloat16().cuda() for a in (q, k, v))
+    qf, kf, vf = (bf16_round(a) for a in (q, k, v))
+    p = gpu.PipelineParams(q_clusters=65, topk=25, full_layer_quota=0.0)
+    op = oracle.Params(q_clusters=65, topk=25, full_layer_quota=0.0)
+    out, hs = gpu.adacluster_attention(qb, kb, vb, gpu.LayerPolicy(topk=25), gpu.StepState(), 0, p)
+    r = oracle.head_step(qf, kf, vf, None, oracle.HeadState(), 0, op)
+    assert np.array_equal(hs.key_model.assignments.cpu().numpy(), r.key_model.assignments)
+    assert np.array_equal(hs.q_model.assignments.cpu().numpy(), r.q_model.assignments)
+    assert np.array_equal(hs.selection.selected.cpu().numpy(), r.selection.selected)
+    assert rel_l2(r.out, out.float().cpu().numpy()) <= BF16_TOL
+
+
+def _steps_inputs(seed, steps=3, layers=2, heads=2, L=256, D=8, drift=0.0, sigma=0.3):
+    out = []
+    for l in range(layers):
+        spec = LayerSpec(kind="compact", gaussian_components=8, component_sigma=sigma,
+                         component_separation=15.0, drift_sigma=drift)
+        out.append(gen_synthetic(spec, L, D, heads, steps, seed + l))
+    return [[out[l][t] for l in range(layers)] for t in range(steps)]
+
+
+@pytest.mark.parametrize("seed,steps,drift,quota,layers,heads", [
+    (2, 3, 0.02, 0.15, 2, 2), (4, 2, 0.0, 0.5, 2, 2), (6, 4, 0.02, 0.0, 1, 1),
+])
+def test_run_denoise_steps_vs_oracle(gpu, oracle, seed, steps, drift, quota, layers, heads):
+    inp = _steps_inputs(seed, steps=steps, drift=drift, layers=layers, heads=heads)
+    p = gpu.PipelineParams(q_clusters=8, topk=3, m0=16, n_max=1000, full_layer_quota=quota)
+    op = oracle.Params(q_clusters=8, topk=3, m0=16, n_max=1000, full_layer_quota=quota)
+    res = gpu.run_denoise_steps(inp, p, seed=1)
+    outs, modes, rr, mse, _ = oracle.run_steps(inp, op, seed=1)
+    assert [pl.mode for pl in res.policies] == modes
+    assert res.mse_layer == mse
+    for t in range(steps):
+        for l in range(layers):
+            for h in range(heads):
+                hs, r = res.stats[t][l][h], rr[t][l][h]
+                assert hs.mode == r.mode
+                assert rel_l2(outs[t][l][h], res.outputs[t][l][h]) <= F32_TOL
+                if hs.mode == "sparse":
+                    assert np.array_equal(hs.selection.selected, r.selection.selected)
+                    assert hs.key_iters == r.key_iters
+                    assert hs.query_iters == r.query_iters
+                    assert hs.density == r.selection.density
