@@ -263,16 +263,30 @@ int ac_build_q_layout(const void* q, int dtype, int d, int64_t L, int heads,
  * head.  Keys/values are in cluster-contiguous order (Kp/Vp, member order);
  * the item attends over the union of [start,end) runs of Kp.               */
 
-/* q:  Qp [total_q_rows, d] (dtype), rows grouped per item
- * qidx: [total_q_rows] original token index of each Qp row (-1 = padding)
+/* q:  Qp [q_rows_total, d] (dtype), rows grouped per item
+ * qidx: [q_rows_total] original token index of each Qp row (-1 = padding)
  * k/v: Kp/Vp [heads, L, d] (dtype), runs: [*, 2] int32 ranges into [0, L)
  * out: [heads, L, d] f32 or bf16 (out_dtype), written at original rows.
- * scale: softmax scale (1/sqrt(d) in the reference, reference.py:39).     */
-int ac_sparse_attention(const void* q, const int32_t* qidx, const void* k,
-                        const void* v, int dtype, int d, int64_t L,
-                        const ac_attn_item* items, int nitems,
+ * scale: softmax scale (1/sqrt(d) in the reference, reference.py:39).
+ * bf16 inputs with d in {64, 128} run on the tcgen05 kernel; everything else
+ * (f32 inputs: the 1e-4 parity bar needs f32 math) on the CUDA-core kernel. */
+int ac_sparse_attention(const void* q, int64_t q_rows_total, const int32_t* qidx,
+                        const void* k, const void* v, int dtype, int d, int64_t L,
+                        int heads, const ac_attn_item* items, int nitems,
                         const int32_t* runs, float scale, void* out,
                         int out_dtype, void* stream);
+/* explicit kernels (tests / benchmarks) */
+int ac_sparse_attention_simt(const void* q, const int32_t* qidx, const void* k,
+                             const void* v, int dtype, int d, int64_t L,
+                             const ac_attn_item* items, int nitems,
+                             const int32_t* runs, float scale, void* out,
+                             int out_dtype, void* stream);
+int ac_sparse_attention_tc(const void* q, int64_t q_rows_total,
+                           const int32_t* qidx, const void* k, const void* v,
+                           int d, int64_t L, int heads,
+                           const ac_attn_item* items, int nitems,
+                           const int32_t* runs, float scale, void* out,
+                           int out_dtype, void* stream);
 
 #ifdef __cplusplus
 }

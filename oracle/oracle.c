@@ -14,9 +14,49 @@
  * load this library.  Built by oracle/Makefile into oracle/_build/.
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
+
+/* ---- row-parallel helper: rows are independent, so splitting them across
+ * threads leaves every value bit-identical ----------------------------- */
+typedef void (*row_fn)(void* ctx, int64_t lo, int64_t hi);
+typedef struct { row_fn fn; void* ctx; int64_t lo, hi; } par_job;
+static int g_threads = 0;
+int oc_num_threads(void) {
+  if (g_threads <= 0) {
+    const char* e = getenv("ORACLE_THREADS");
+    long t = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+    g_threads = (int)(t < 1 ? 1 : (t > 256 ? 256 : t));
+  }
+  return g_threads;
+}
+void oc_set_threads(int t) { g_threads = t; }
+static void* par_entry(void* p) {
+  par_job* j = (par_job*)p;
+  j->fn(j->ctx, j->lo, j->hi);
+  return NULL;
+}
+static void par_rows(int64_t n, row_fn fn, void* ctx) {
+  int T = oc_num_threads();
+  if (n < 4096 || T == 1) { fn(ctx, 0, n); return; }
+  if (T > 256) T = 256;
+  pthread_t th[256];
+  par_job jobs[256];
+  const int64_t per = (n + T - 1) / T;
+  int used = 0;
+  for (int t = 0; t < T; ++t) {
+    const int64_t lo = t * per, hi = lo + per < n ? lo + per : n;
+    if (lo >= hi) break;
+    jobs[t] = (par_job){fn, ctx, lo, hi};
+    ++used;
+  }
+  for (int t = 1; t < used; ++t) pthread_create(&th[t], NULL, par_entry, &jobs[t]);
+  par_entry(&jobs[0]);
+  for (int t = 1; t < used; ++t) pthread_join(th[t], NULL);
+}
 
 #define ORD_SEQ 0
 #define ORD_L16 1
@@ -146,29 +186,48 @@ static float np_min(float a, float b) { return (a <= b || isnan(a)) ? a : b; }
 
 /* clustering.py:68-75 + :94-97.  labels/best (assigned squared distance);
  * dfull optional [n, k].  `order` < 0 selects the reference's dispatch. */
+typedef struct {
+  const float *x, *c, *cc;
+  int64_t n;
+  int d, k, order;
+  int32_t* labels;
+  float *best, *dfull;
+} assign_ctx;
+
+static void assign_rows(void* p, int64_t lo, int64_t hi) {
+  const assign_ctx* a = (const assign_ctx*)p;
+  const int d = a->d, k = a->k;
+  const int64_t n = a->n;
+  float* tmp = (float*)malloc(sizeof(float) * d);
+  for (int64_t i = lo; i < hi; ++i) {
+    const float* xr = a->x + i * d;
+    const float xx = rowsq(xr, d, tmp);
+    float bd = INFINITY;
+    int bl = -1;
+    for (int j = 0; j < k; ++j) {
+      const int hv = (i >= n - n % 4) && (j >= k - k % 4);
+      const float xc = dot_ord(xr, a->c + (int64_t)j * d, d, a->order, hv);
+      float dd = (xx - 2.0f * xc) + a->cc[j];
+      dd = np_max(dd, 0.f);
+      if (a->dfull) a->dfull[i * k + j] = dd;
+      if (bl < 0 || dd < bd) { bd = dd; bl = j; }
+    }
+    a->labels[i] = bl;
+    a->best[i] = bd;
+  }
+  free(tmp);
+}
+
 void oc_assign(const float* x, int64_t n, int d, const float* c, int k, int order,
                int32_t* labels, float* best, float* dfull) {
   if (order < 0) order = oc_gemm_order(n, k, d);
   float* tmp = (float*)malloc(sizeof(float) * d);
   float* cc = (float*)malloc(sizeof(float) * (k > 0 ? k : 1));
   for (int j = 0; j < k; ++j) cc[j] = rowsq(c + (int64_t)j * d, d, tmp);
-  for (int64_t i = 0; i < n; ++i) {
-    const float xx = rowsq(x + i * d, d, tmp);
-    float bd = INFINITY;
-    int bl = -1;
-    for (int j = 0; j < k; ++j) {
-      const int hv = (i >= n - n % 4) && (j >= k - k % 4);
-      const float xc = dot_ord(x + i * d, c + (int64_t)j * d, d, order, hv);
-      float dd = (xx - 2.0f * xc) + cc[j];
-      dd = np_max(dd, 0.f);
-      if (dfull) dfull[i * k + j] = dd;
-      if (bl < 0 || dd < bd) { bd = dd; bl = j; }
-    }
-    labels[i] = bl;
-    best[i] = bd;
-  }
-  free(cc);
   free(tmp);
+  assign_ctx a = {x, c, cc, n, d, k, order, labels, best, dfull};
+  par_rows(n, assign_rows, &a);
+  free(cc);
 }
 
 /* clustering.py:100-116 on the assigned distances.  Returns repairs done. */
@@ -193,16 +252,6 @@ static int repair_empty(const float* x, int64_t n, int d, float* centers, int k,
   memset(counts, 0, sizeof(int64_t) * k);
   for (int64_t i = 0; i < n; ++i) counts[labels[i]]++;
   return repairs;
-}
-
-/* stable argsort of labels (counting sort) -> order, starts */
-static void stable_order(const int32_t* labels, int64_t n, int k, const int64_t* counts,
-                         int64_t* order, int64_t* starts) {
-  int64_t* pos = (int64_t*)malloc(sizeof(int64_t) * (k > 0 ? k : 1));
-  int64_t acc = 0;
-  for (int j = 0; j < k; ++j) { starts[j] = acc; pos[j] = acc; acc += counts[j]; }
-  for (int64_t i = 0; i < n; ++i) order[pos[labels[i]]++] = i;
-  free(pos);
 }
 
 /* f64 mean of members in member order (np.add.reduceat / np.add.at) */
@@ -263,6 +312,29 @@ int oc_lloyd(const float* x, int64_t n, int d, float* centers, int k, int max_it
   return n_iter;
 }
 
+typedef struct {
+  const float* x;
+  const float* c;
+  float* closest;
+  int d, init;
+} kpp_ctx;
+
+/* closest = min(closest, ((x - c) ** 2).sum(axis=1)) over a row range */
+static void kpp_rows(void* p, int64_t lo, int64_t hi) {
+  const kpp_ctx* a = (const kpp_ctx*)p;
+  const int d = a->d;
+  float* tmp = (float*)malloc(sizeof(float) * d);
+  for (int64_t i = lo; i < hi; ++i) {
+    for (int t = 0; t < d; ++t) {
+      const float df = a->x[i * d + t] - a->c[t];
+      tmp[t] = df * df;
+    }
+    const float v = pw_f_s(tmp, d, 1);
+    a->closest[i] = a->init ? v : np_min(a->closest[i], v);
+  }
+  free(tmp);
+}
+
 /* clustering.py:78-91.  draws[0] = first index, draws[i] = u_i or -(idx+1)
  * (forced rng.integers result).  Returns -1, or the step i at which
  * `total <= 0` was met with an unforced draw (centres [0, i) are valid). */
@@ -272,13 +344,8 @@ int oc_kmeanspp(const float* x, int64_t n, int d, int k, const double* draws, fl
   double* cdf = (double*)malloc(sizeof(double) * n);
   int64_t idx = (int64_t)draws[0];
   memcpy(centers, x + idx * d, sizeof(float) * d);
-  for (int64_t i = 0; i < n; ++i) {
-    for (int t = 0; t < d; ++t) {
-      const float df = x[i * d + t] - centers[t];
-      tmp[t] = df * df;
-    }
-    closest[i] = pw_f_s(tmp, d, 1);
-  }
+  kpp_ctx kc = {x, centers, closest, d, 1};
+  par_rows(n, kpp_rows, &kc);
   int stop = -1;
   for (int s = 1; s < k; ++s) {
     const float total = pw_f_s(closest, n, 1);
@@ -299,13 +366,9 @@ int oc_kmeanspp(const float* x, int64_t n, int d, int k, const double* draws, fl
       if (idx >= n) idx = n - 1;
     }
     memcpy(centers + (int64_t)s * d, x + idx * d, sizeof(float) * d);
-    for (int64_t i = 0; i < n; ++i) {
-      for (int t = 0; t < d; ++t) {
-        const float df = x[i * d + t] - centers[(int64_t)s * d + t];
-        tmp[t] = df * df;
-      }
-      closest[i] = np_min(closest[i], pw_f_s(tmp, d, 1));
-    }
+    kc.c = centers + (int64_t)s * d;
+    kc.init = 0;
+    par_rows(n, kpp_rows, &kc);
   }
   free(cdf);
   free(tmp);
@@ -432,3 +495,4 @@ void oc_scores(const float* reps, int gq, int d, const float* emax, const float*
   free(qb);
   free(qa);
 }
+

@@ -273,8 +273,9 @@ k_assign_seq(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int
   }
   if (count) {
     __syncthreads();
-    int32_t* th = P.tile_hist + (int64_t)blockIdx.x * k;
-    for (int c = tid; c < k; c += blockDim.x) th[c] = s_hist[c];
+    const int64_t ntiles = (n + kAsgBM - 1) / kAsgBM;
+    int32_t* th = P.tile_hist + blockIdx.x;
+    for (int c = tid; c < k; c += blockDim.x) th[(int64_t)c * ntiles] = s_hist[c];
   }
 }
 
@@ -320,8 +321,9 @@ __global__ void k_assign_generic(const ac_cluster_problem* __restrict__ probs, i
   }
   if (count) {
     __syncthreads();
-    int32_t* th = P.tile_hist + (int64_t)blockIdx.x * k;
-    for (int c = threadIdx.x; c < k; c += blockDim.x) th[c] = s_hist[c];
+    const int64_t ntiles = (n + kAsgBM - 1) / kAsgBM;
+    int32_t* th = P.tile_hist + blockIdx.x;
+    for (int c = threadIdx.x; c < k; c += blockDim.x) th[(int64_t)c * ntiles] = s_hist[c];
   }
 }
 
@@ -337,8 +339,9 @@ __global__ void k_tile_hist(const ac_cluster_problem* __restrict__ probs, int kc
   __syncthreads();
   if ((int)threadIdx.x < rows) atomicAdd(&thsm[P.labels[row0 + threadIdx.x]], 1);
   __syncthreads();
-  int32_t* th = P.tile_hist + (int64_t)blockIdx.x * k;
-  for (int c = threadIdx.x; c < k; c += blockDim.x) th[c] = thsm[c];
+  const int64_t ntiles = (P.n + kAsgBM - 1) / kAsgBM;
+  int32_t* th = P.tile_hist + blockIdx.x;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) th[(int64_t)c * ntiles] = thsm[c];
 }
 
 // ---------------------------------------------------------------------------
@@ -352,26 +355,25 @@ __global__ void k_hist_scan(const ac_cluster_problem* __restrict__ probs, int fl
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (!(flags & AC_ASSIGN_ALL) && P.status[AC_ST_ACTIVE] == 0) return;
   const int k = P.k;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= k) return;
   const int tiles = (int)((P.n + kAsgBM - 1) / kAsgBM);
-  int32_t* h = P.tile_hist + c;
+  int32_t* h = P.tile_hist + (int64_t)c * tiles;  // this label's row, contiguous over tiles
   int run = 0;
-  int t = 0;
-  for (; t + 4 <= tiles; t += 4) {
-    const int v0 = h[(int64_t)(t + 0) * k], v1 = h[(int64_t)(t + 1) * k];
-    const int v2 = h[(int64_t)(t + 2) * k], v3 = h[(int64_t)(t + 3) * k];
-    h[(int64_t)(t + 0) * k] = run; run += v0;
-    h[(int64_t)(t + 1) * k] = run; run += v1;
-    h[(int64_t)(t + 2) * k] = run; run += v2;
-    h[(int64_t)(t + 3) * k] = run; run += v3;
+  for (int t0 = 0; t0 < tiles; t0 += 32) {
+    const int t = t0 + lane;
+    const int v = (t < tiles) ? h[t] : 0;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (t < tiles) h[t] = run + inc - v;
+    run += __shfl_sync(0xffffffffu, inc, 31);
   }
-  for (; t < tiles; ++t) {
-    const int v = h[(int64_t)t * k];
-    h[(int64_t)t * k] = run;
-    run += v;
-  }
-  P.counts[c] = run;
+  if (lane == 0) P.counts[c] = run;
 }
 
 // _repair_empty (clustering.py:100-116) + inertia (:132) + segment starts.
@@ -436,8 +438,8 @@ k_post(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int iter,
     const int tiles = (int)((n + kAsgBM - 1) / kAsgBM);
     const int ft = (int)(far / kAsgBM);
     for (int t = ft + 1 + tid; t < tiles; t += blockDim.x) {
-      P.tile_hist[(int64_t)t * k + old] -= 1;
-      P.tile_hist[(int64_t)t * k + c] += 1;
+      P.tile_hist[(int64_t)old * tiles + t] -= 1;
+      P.tile_hist[(int64_t)c * tiles + t] += 1;
     }
     __syncthreads();
   }
@@ -488,113 +490,129 @@ __global__ void k_scatter(const ac_cluster_problem* __restrict__ probs, int flag
     const int l = s_lab[tid];
     int rank = 0;
     for (int j = 0; j < tid; ++j) rank += (s_lab[j] == l);
-    const int pos = P.starts[l] + P.tile_hist[(int64_t)blockIdx.x * P.k + l] + rank;
+    const int64_t ntiles = (P.n + kAsgBM - 1) / kAsgBM;
+    const int pos = P.starts[l] + P.tile_hist[(int64_t)l * ntiles + blockIdx.x] + rank;
     P.perm[pos] = (int32_t)(row0 + tid);
   }
 }
 
 // ---------------------------------------------------------------------------
-// K4: centroid update (clustering.py:133-143).  One warp per centre: the f64
-// sum runs over the members in stable label order exactly like
-// np.add.reduceat(x[order].astype(f64), starts), then / count -> f32.
-// The same warp computes the f32 movement norm and the new ||c||^2; the last
-// warp of a problem reduces the movement mean and clears the active flag when
-// movement < tol.
+// K4: centroid update (clustering.py:133-143).  One CTA per centre: member
+// rows (in stable label order) are staged through shared memory with
+// cp.async double buffering so ~64 rows are in flight; thread t < D owns the
+// f64 chain of dimension t and adds the members in order, exactly like
+// np.add.reduceat(x[order].astype(f64), starts) (first row initialises).
+// Then / count -> f32, the f32 movement norm and the new ||c||^2; the last
+// CTA of a problem reduces the movement mean and clears `active` when
+// movement < tol.  mode 1 = segment mean into outs[p] (query reps).
 // ---------------------------------------------------------------------------
-constexpr int kMaxDimPerLane = 8;  // D <= 256
+constexpr int kUpdRows = 64;
+
+AC_DEV void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+AC_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+AC_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+__host__ __device__ inline size_t update_smem_bytes(int d, int dtype) {
+  const size_t rb = (size_t)d * (dtype == AC_DTYPE_BF16 ? 2 : 4);
+  return 2 * kUpdRows * ((rb + 15) / 16 * 16) + sizeof(float) * 2 * (size_t)d + 16;
+}
 
 __global__ void __launch_bounds__(256)
 k_update(const ac_cluster_problem* __restrict__ probs, int dtype, int d, double tol,
          int mode /*0 = lloyd update, 1 = segment mean into out*/, float* const* outs) {
-  extern __shared__ __align__(16) float usm[];
+  extern __shared__ __align__(16) unsigned char usm[];
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (mode == 0 && P.status[AC_ST_ACTIVE] == 0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * (blockDim.x >> 5) + warp;
+  const int c = blockIdx.x;
   const int k = P.k;
-  float* sq = usm + warp * 2 * d;  // [2][d] scratch per warp
-  const bool valid = c < k;
-  if (valid) {
-    const int cnt = P.counts[c];
-    const int s0 = P.starts[c];
-    double acc[kMaxDimPerLane];
-#pragma unroll
-    for (int j = 0; j < kMaxDimPerLane; ++j) acc[j] = 0.0;
-    const int nper = (d + 31) >> 5;
-    // first member initialises (reduceat copies the first row), the rest add in order
-    int m = 0;
-    constexpr int U = 4;
-    for (; m + U <= cnt; m += U) {
-      int64_t rows[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) rows[u] = P.perm[s0 + m + u];
-      float v[U][kMaxDimPerLane];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int j = 0; j < kMaxDimPerLane; ++j) {
-          const int t = lane + 32 * j;
-          v[u][j] = (j < nper && t < d) ? ld_elem(P.x, dtype, rows[u] * d + t) : 0.f;
-        }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int j = 0; j < kMaxDimPerLane; ++j)
-          acc[j] = (m + u == 0) ? (double)v[u][j] : __dadd_rn(acc[j], (double)v[u][j]);
-    }
-    for (; m < cnt; ++m) {
-      const int64_t row = P.perm[s0 + m];
-#pragma unroll
-      for (int j = 0; j < kMaxDimPerLane; ++j) {
-        const int t = lane + 32 * j;
-        const float v = (j < nper && t < d) ? ld_elem(P.x, dtype, row * d + t) : 0.f;
-        acc[j] = (m == 0) ? (double)v : __dadd_rn(acc[j], (double)v);
+  if (c >= k) return;
+  const int tid = threadIdx.x;
+  const int esz = dtype == AC_DTYPE_BF16 ? 2 : 4;
+  const int row_bytes = d * esz;
+  const int rbp = (row_bytes + 15) / 16 * 16;
+  unsigned char* buf0 = usm;
+  unsigned char* buf1 = usm + (size_t)kUpdRows * rbp;
+  float* sq = reinterpret_cast<float*>(usm + 2 * (size_t)kUpdRows * rbp);
+  const int cnt = P.counts[c], s0 = P.starts[c];
+  const char* xb = reinterpret_cast<const char*>(P.x);
+  const bool vec = (row_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(P.x) & 15) == 0);
+  const int nchunks = (cnt + kUpdRows - 1) / kUpdRows;
+
+  auto issue = [&](int chunk, unsigned char* dst) {
+    const int m0 = chunk * kUpdRows;
+    const int rows = min(kUpdRows, cnt - m0);
+    if (vec) {
+      const int vpr = row_bytes / 16;
+      for (int e = tid; e < rows * vpr; e += blockDim.x) {
+        const int r = e / vpr, part = e - r * vpr;
+        const int64_t row = P.perm[s0 + m0 + r];
+        cp_async16(dst + (size_t)r * rbp + part * 16, xb + row * row_bytes + part * 16);
+      }
+    } else {
+      for (int e = tid; e < rows * d; e += blockDim.x) {
+        const int r = e / d, t = e - r * d;
+        const int64_t row = P.perm[s0 + m0 + r];
+        if (esz == 2)
+          reinterpret_cast<__nv_bfloat16*>(dst + (size_t)r * rbp)[t] =
+              reinterpret_cast<const __nv_bfloat16*>(P.x)[row * d + t];
+        else
+          reinterpret_cast<float*>(dst + (size_t)r * rbp)[t] =
+              reinterpret_cast<const float*>(P.x)[row * d + t];
       }
     }
-    const double dc = (double)cnt;
-    float* dst = (mode == 0) ? P.centers + (int64_t)c * d : outs[blockIdx.y] + (int64_t)c * d;
-#pragma unroll
-    for (int j = 0; j < kMaxDimPerLane; ++j) {
-      const int t = lane + 32 * j;
-      if (j < nper && t < d) {
-        const float nv = __double2float_rn(__ddiv_rn(acc[j], dc));
-        if (mode == 0) {
-          const float ov = dst[t];
-          const float df = __fsub_rn(nv, ov);
-          sq[t] = __fmul_rn(df, df);
-          sq[d + t] = __fmul_rn(nv, nv);
-        }
-        dst[t] = nv;
+    cp_async_commit();
+  };
+
+  double acc = 0.0;
+  if (nchunks > 0) issue(0, buf0);
+  for (int j = 0; j < nchunks; ++j) {
+    unsigned char* cur = (j & 1) ? buf1 : buf0;
+    if (j + 1 < nchunks) issue(j + 1, (j & 1) ? buf0 : buf1);
+    else cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    if (tid < d) {
+      const int rows = min(kUpdRows, cnt - j * kUpdRows);
+      for (int r = 0; r < rows; ++r) {
+        const unsigned char* rp = cur + (size_t)r * rbp;
+        const float v = (esz == 2) ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rp)[tid])
+                                   : reinterpret_cast<const float*>(rp)[tid];
+        acc = (j == 0 && r == 0) ? (double)v : __dadd_rn(acc, (double)v);
       }
     }
-    __syncwarp();
-    if (mode == 0 && lane == 0) {
-      const float* a = sq;
-      const float* b = sq + d;
-      P.movement[c] = __fsqrt_rn(pw_sum<float>([&](int i) { return a[i]; }, d));
-      P.cc[c] = pw_sum<float>([&](int i) { return b[i]; }, d);
+    __syncthreads();
+  }
+  float* dst = (mode == 0) ? P.centers + (int64_t)c * d : outs[blockIdx.y] + (int64_t)c * d;
+  if (tid < d) {
+    const float nv = __double2float_rn(__ddiv_rn(acc, (double)cnt));
+    if (mode == 0) {
+      const float df = __fsub_rn(nv, dst[tid]);
+      sq[tid] = __fmul_rn(df, df);
+      sq[d + tid] = __fmul_rn(nv, nv);
     }
+    dst[tid] = nv;
   }
   if (mode != 0) return;
-  // completion counting per problem (one arrival per warp that owns a centre)
-  __shared__ int s_last[8];
-  if (lane == 0) {
-    s_last[warp] = 0;
-    if (valid) {
-      __threadfence();
-      const int prev = atomicAdd(&P.status[AC_ST_DONE], 1);
-      s_last[warp] = (prev == k - 1);
-    }
-  }
-  __syncwarp();
-  if (valid && s_last[warp] && lane == 0) {
+  __syncthreads();
+  if (tid == 0) {
+    const float* a = sq;
+    const float* b = sq + d;
+    P.movement[c] = __fsqrt_rn(pw_sum<float>([&](int i) { return a[i]; }, d));
+    P.cc[c] = pw_sum<float>([&](int i) { return b[i]; }, d);
     __threadfence();
-    const volatile float* mv = P.movement;
-    const float s = pw_sum<float>([&](int i) { return mv[i]; }, k);
-    const float mean = __double2float_rn(__ddiv_rn((double)s, (double)k));
-    P.status[AC_ST_DONE] = 0;
-    P.status[AC_ST_NITER] += 1;
-    if ((double)mean < tol) P.status[AC_ST_ACTIVE] = 0;
+    const int prev = atomicAdd(&P.status[AC_ST_DONE], 1);
+    if (prev == k - 1) {
+      __threadfence();
+      const volatile float* mv = P.movement;
+      const float s = pw_sum<float>([&](int i) { return mv[i]; }, k);
+      const float mean = __double2float_rn(__ddiv_rn((double)s, (double)k));
+      P.status[AC_ST_DONE] = 0;
+      P.status[AC_ST_NITER] += 1;
+      if ((double)mean < tol) P.status[AC_ST_ACTIVE] = 0;
+    }
   }
 }
 
@@ -981,7 +999,7 @@ extern "C" int ac_assign(const ac_cluster_problem* probs, int nprob, int dtype, 
 static int repair_sort_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
                             int64_t max_n, int max_k, int iter, int flags, cudaStream_t st) {
   const unsigned tiles = (unsigned)((max_n + kAsgBM - 1) / kAsgBM);
-  k_hist_scan<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, flags);
+  k_hist_scan<<<dim3((max_k + 7) / 8, nprob), 256, 0, st>>>(probs, flags);
   const size_t psm = plan_vals_bytes(max_n, sizeof(float));
   int rc = set_smem((const void*)k_post, psm);
   if (rc) return rc;
@@ -999,12 +1017,11 @@ extern "C" int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dt
 
 static int update_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d, int max_k,
                        double tol, int mode, float* const* outs, cudaStream_t st) {
-  const int warps = 8;
-  const size_t smem = sizeof(float) * warps * 2 * d;
+  if (d > 256) { ac_host::set_error("update: d=%d > 256", d); return AC_ERR_DIM; }
+  const size_t smem = update_smem_bytes(d, dtype);
   int rc = set_smem((const void*)k_update, smem);
   if (rc) return rc;
-  k_update<<<dim3((max_k + warps - 1) / warps, nprob), warps * 32, smem, st>>>(probs, dtype, d, tol,
-                                                                               mode, outs);
+  k_update<<<dim3(max_k, nprob), 256, smem, st>>>(probs, dtype, d, tol, mode, outs);
   AC_CHECK_LAUNCH("k_update");
   return AC_OK;
 }

@@ -24,6 +24,7 @@ import torch
 
 from . import _lib as L
 from .errors import DimensionError, ParameterError
+from .profiling import phase
 
 F32 = torch.float32
 I32 = torch.int32
@@ -623,10 +624,17 @@ def sparse_attention_heads(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
            qcounts.data_ptr(), qlab.data_ptr(), gq.data_ptr(), gq_max, nruns.data_ptr(), topk_max,
            qp.data_ptr(), qidx.data_ptr(), qp_cap, items.data_ptr(), item_cap, L.stream_ptr())
     out = torch.empty((H, Ln, da), dtype=out_dtype, device=dev)
-    fn = "ac_sparse_attention" if impl == "auto" else "ac_sparse_attention_simt"
-    L.call(fn, qp.data_ptr(), qidx.data_ptr(), kp.data_ptr(), vp.data_ptr(), dt, da, Ln,
-           items.data_ptr(), H * item_cap, runs.data_ptr(), float(1.0 / math.sqrt(D)),
-           out.data_ptr(), L.dtype_code(out) if out_dtype != F32 else L.DTYPE_F32, L.stream_ptr())
+    odt = L.dtype_code(out) if out_dtype != F32 else L.DTYPE_F32
+    scale = float(1.0 / math.sqrt(D))
+    with phase("attention"):
+        if impl == "simt":
+            L.call("ac_sparse_attention_simt", qp.data_ptr(), qidx.data_ptr(), kp.data_ptr(),
+                   vp.data_ptr(), dt, da, Ln, items.data_ptr(), H * item_cap, runs.data_ptr(),
+                   scale, out.data_ptr(), odt, L.stream_ptr())
+        else:
+            L.call("ac_sparse_attention", qp.data_ptr(), H * qp_cap, qidx.data_ptr(),
+                   kp.data_ptr(), vp.data_ptr(), dt, da, Ln, H, items.data_ptr(), H * item_cap,
+                   runs.data_ptr(), scale, out.data_ptr(), odt, L.stream_ptr())
     return out[..., :D] if da != D else out
 
 

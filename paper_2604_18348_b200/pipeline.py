@@ -22,12 +22,13 @@ from . import _lib as L
 from . import engine as E
 from .clustering import ClusterModel, export_model
 from .errors import ContractError, ParameterError
+from .profiling import phase
 from .quest import SelectionResult
 from .tensorops import to_device, to_host
 
 __all__ = ["PipelineParams", "LayerPolicy", "StepState", "HeadStats", "FlopCounts",
            "count_flops", "clustering_flops", "adacluster_attention", "run_denoise_steps",
-           "DenoiseResult", "LayerRunner"]
+           "DenoiseResult", "LayerRunner", "LayerSession"]
 
 SCORERS = ("quest", "mean", "clamped")
 
@@ -150,24 +151,29 @@ class LayerRunner:
         H, Ln, _ = Q.shape
         qs = [Q[h] for h in range(H)]
         ks = [K[h] for h in range(H)]
-        qm, reps, _ = E.cluster_queries_batch(qs, [min(p.q_clusters, Ln)] * H, seeds, p.max_iter,
-                                              p.tol)
+        with phase("plan_queries"):
+            qm, reps, _ = E.cluster_queries_batch(qs, [min(p.q_clusters, Ln)] * H, seeds,
+                                                  p.max_iter, p.tol)
         if p.uniform_key_clusters is not None:
             km = E.kmeans_batch(ks, [min(p.uniform_key_clusters, Ln)] * H, seeds, p.max_iter, p.tol)
             return LayerPlan(qm, reps, km, [None] * H)
         m0 = min(p.m0, Ln)
-        s0 = E.kmeans_batch(ks, [m0] * H, seeds, p.max_iter, p.tol)
-        taus = [float(t) for t in E.tau_batch(ks, s0, p.tau_factor).cpu().numpy()]
-        km = E.multi_stage_batch(ks, taus, p.n_max, m0, seeds, p.max_iter, p.tol, s0)
+        with phase("plan_stage0"):
+            s0 = E.kmeans_batch(ks, [m0] * H, seeds, p.max_iter, p.tol)
+            taus = [float(t) for t in E.tau_batch(ks, s0, p.tau_factor).cpu().numpy()]
+        with phase("plan_multistage"):
+            km = E.multi_stage_batch(ks, taus, p.n_max, m0, seeds, p.max_iter, p.tol, s0)
         return LayerPlan(qm, reps, km, taus)
 
     def warm(self, Q: torch.Tensor, K: torch.Tensor, key_centers: list, query_centers: list):
         """Warm-started clusterings of a later step (pipeline.py:263-267)."""
         p = self.p
         H = Q.shape[0]
-        km = E.lloyd_batch([K[h] for h in range(H)], key_centers, p.max_iter, p.tol)
-        qm, reps, _ = E.cluster_queries_batch([Q[h] for h in range(H)], [0] * H, [0] * H,
-                                              p.max_iter, p.tol, inits=query_centers)
+        with phase("warm_keys"):
+            km = E.lloyd_batch([K[h] for h in range(H)], key_centers, p.max_iter, p.tol)
+        with phase("warm_queries"):
+            qm, reps, _ = E.cluster_queries_batch([Q[h] for h in range(H)], [0] * H, [0] * H,
+                                                  p.max_iter, p.tol, inits=query_centers)
         return qm, reps, km
 
     def sparse(self, Q, K, V, q_models, reps, key_models, topk: int) -> SparseOut:
@@ -175,14 +181,15 @@ class LayerRunner:
         p = self.p
         H = Q.shape[0]
         ks = [K[h] for h in range(H)]
-        if p.scorer == "quest":
-            emax, emin = E.envelopes_batch(ks, key_models)
-        else:
-            emax = emin = [m.centers for m in key_models]
-        topks = [min(topk, m.k) for m in key_models]
-        sels, runs, nruns = E.select_batch(reps, emax, emin, key_models, topks, p.scorer)
-        out = E.sparse_attention_heads(Q, K, V, q_models, key_models, runs, nruns, self.out_dtype,
-                                       self.attn_impl)
+        with phase("select"):
+            if p.scorer == "quest":
+                emax, emin = E.envelopes_batch(ks, key_models)
+            else:
+                emax = emin = [m.centers for m in key_models]
+            topks = [min(topk, m.k) for m in key_models]
+            sels, runs, nruns = E.select_batch(reps, emax, emin, key_models, topks, p.scorer)
+        out = E.sparse_attention_heads(Q, K, V, q_models, key_models, runs, nruns,
+                                       self.out_dtype, self.attn_impl)
         return SparseOut(out, sels, topks)
 
     def dense(self, Q, K, V) -> torch.Tensor:
@@ -192,8 +199,9 @@ class LayerRunner:
         """_carry_centers at step 0 (pipeline.py:223-234): one warm Lloyd."""
         p = self.p
         H = K.shape[0]
-        return E.lloyd_batch([K[h] for h in range(H)], [m.centers for m in key_models], p.max_iter,
-                             p.tol)
+        with phase("consolidate"):
+            return E.lloyd_batch([K[h] for h in range(H)], [m.centers for m in key_models],
+                                 p.max_iter, p.tol)
 
 
 def _stack(heads, keep_bf16=True):
@@ -383,3 +391,65 @@ def run_denoise_steps(step_inputs, params: PipelineParams | None = None, seed: i
         outputs.append(s_out)
         stats.append(s_stats)
     return DenoiseResult(outputs=outputs, policies=policies, stats=stats, mse_layer=mse_layer)
+
+
+class LayerSession:
+    """Stateful driver of one layer across denoising steps (the streamed form
+    of ``run_denoise_steps`` for a single layer).  ``step(Q, K, V)`` takes
+    [H, L, D] tensors (CUDA, or host/pinned — then the copies are part of the
+    call) and returns [H, L, D] outputs (on the inputs' side).  Step 0 plans
+    every head and fixes the layer policy (any flagged head -> full, as the
+    reference's per-layer rule with quota 0); later steps warm-start."""
+
+    def __init__(self, params: PipelineParams | None = None, seed: int = 0, layer: int = 0,
+                 out_dtype=None, attn_impl: str = "auto", head_offset: int = 0):
+        self.params = params or PipelineParams()
+        self.params.validate()
+        self.seed, self.layer, self.head_offset = seed, layer, head_offset
+        self.out_dtype = out_dtype
+        self.attn_impl = attn_impl
+        self.t = 0
+        self.mode = None
+        self.key_centers = None
+        self.query_centers = None
+        self.last = None
+
+    def step(self, Q, K, V):
+        host = not (isinstance(Q, torch.Tensor) and Q.device.type == "cuda")
+        dev = L.device()
+        if host:
+            Q, K, V = (torch.as_tensor(x).to(dev, non_blocking=True) for x in (Q, K, V))
+        odt = self.out_dtype or (torch.bfloat16 if Q.dtype == torch.bfloat16 else torch.float32)
+        run = LayerRunner(self.params, odt, self.attn_impl)
+        H = Q.shape[0]
+        if self.t == 0:
+            seeds = [self.seed + 7919 * self.layer + self.head_offset + h for h in range(H)]
+            plan = run.plan(Q, K, seeds)
+            self.mode = "full" if any(m.flag_full for m in plan.key_models) else "sparse"
+            if self.mode == "sparse":
+                so = run.sparse(Q, K, V, plan.q_models, plan.reps, plan.key_models,
+                                self.params.topk)
+                cons = run.consolidate(K, plan.key_models)
+                self.key_centers = [m.centers for m in cons]
+                self.query_centers = [m.centers for m in plan.q_models]
+                self.last = (plan.q_models, plan.key_models, so)
+                out = so.out
+            else:
+                with phase("attention_dense"):
+                    out = run.dense(Q, K, V)
+        elif self.mode == "full":
+            with phase("attention_dense"):
+                out = run.dense(Q, K, V)
+        else:
+            qm, reps, km = run.warm(Q, K, self.key_centers, self.query_centers)
+            so = run.sparse(Q, K, V, qm, reps, km, self.params.topk)
+            self.key_centers = [m.centers for m in km]
+            self.query_centers = [m.centers for m in qm]
+            self.last = (qm, km, so)
+            out = so.out
+        self.t += 1
+        if host:
+            res = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+            res.copy_(out, non_blocking=True)
+            return res
+        return out

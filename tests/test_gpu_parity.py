@@ -222,3 +222,34 @@ def test_run_denoise_steps_vs_oracle(gpu, oracle, seed, steps, drift, quota, lay
                     assert hs.key_iters == r.key_iters
                     assert hs.query_iters == r.query_iters
                     assert hs.density == r.selection.density
+
+
+@pytest.mark.parametrize("H,L,D", [(1, 128, 64), (2, 1000, 64), (3, 4133, 64), (1, 300, 128),
+                                   (2, 2500, 128)])
+def test_dense_attention_tcgen05_bf16(gpu, oracle, H, L, D):
+    """tcgen05 kernel (bf16, D 64/128) vs the f32 oracle on the same bf16 values."""
+    from paper_2604_18348_b200 import engine as E
+    rng = np.random.default_rng(L + D)
+    q, k, v = (rng.normal(size=(H, L, D)).astype(np.float32) for _ in range(3))
+    k *= 2.0
+    qb, kb, vb = (torch.from_numpy(a).bfloat16().cuda() for a in (q, k, v))
+    out = E.dense_attention_heads(qb, kb, vb, out_dtype=torch.float32).cpu().numpy()
+    for h in range(H):
+        ref = oracle.full_attention(*(bf16_round(a[h]) for a in (q, k, v)))
+        assert rel_l2(ref, out[h]) <= BF16_TOL
+
+
+def test_sparse_tcgen05_matches_simt(gpu):
+    """Same runs/items through both attention kernels (bf16 inputs)."""
+    from paper_2604_18348_b200.pipeline import LayerRunner
+    q, k, v = gen_synthetic(CRIT7_SPEC, 6000, 64, 2, 1, 3)[0][0]
+    Q, K, V = (torch.stack([torch.from_numpy(a)] * 2).bfloat16().cuda().contiguous()
+               for a in (q, k, v))
+    p = gpu.PipelineParams(q_clusters=65, topk=25, full_layer_quota=0.0)
+    outs = {}
+    for impl in ("auto", "simt"):
+        run = LayerRunner(p, torch.float32, impl)
+        plan = run.plan(Q, K, [0, 1])
+        so = run.sparse(Q, K, V, plan.q_models, plan.reps, plan.key_models, 25)
+        outs[impl] = so.out.cpu().numpy()
+    assert rel_l2(outs["simt"], outs["auto"]) <= BF16_TOL
