@@ -255,17 +255,13 @@ def main():
         dev_in.append([x.cuda() for x in trip])
     del steps
     params = _params(P)
-    sess = P.LayerSession(params, seed=0, layer=0, head_offset=h0, out_dtype=tdt,
-                          attn_impl=args.attn_impl)
+    from paper_2604_18348_b200.sharding import ShardedLayerSession, gather_heads
+    shard = ShardedLayerSession(H, params, seed=0, layer=0, out_dtype=tdt)
+    sess = shard.session
+    sess.attn_impl = args.attn_impl
 
     def gather(out):
-        if world == 1:
-            return out
-        pad = torch.zeros((per, Ln, D), dtype=out.dtype, device=out.device)
-        pad[:out.shape[0]] = out
-        full = torch.empty((world * per, Ln, D), dtype=out.dtype, device=out.device)
-        dist.all_gather_into_tensor(full, pad)
-        return full[:H]
+        return gather_heads(out, H) if world > 1 else out
 
     def barrier():
         if world > 1:

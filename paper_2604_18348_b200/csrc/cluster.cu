@@ -181,14 +181,18 @@ k_assign_seq(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int
   int* s_hist = s_bi + 8 * kAsgBM;        // [kcap]
 
   const int tid = threadIdx.x;
+  // x tile, transposed: consecutive threads take consecutive rows so the
+  // shared-memory stores are conflict-free
   for (int e = tid; e < kAsgBM * d; e += blockDim.x) {
-    const int r = e / d, t = e - r * d;
+    const int t = e / kAsgBM, r = e - t * kAsgBM;
     xs[t * kAsgPadM + r] = (r < rows) ? ld_elem(P.x, dtype, (row0 + r) * d + t) : 0.f;
   }
   for (int r = tid; r < kAsgBM; r += blockDim.x) s_xx[r] = (r < rows) ? P.xx[row0 + r] : 0.f;
 
-  const int tm = tid & 15;   // rows tm*8 .. tm*8+7
-  const int tn = tid >> 4;   // centres tn*4 .. tn*4+3 of the current 64-block
+  // thread (tm, tn): rows tm*4+i and 64+tm*4+i (i < 4) — two 16-lane-contiguous
+  // float4 reads per k step, conflict-free — and centres tn*4 .. tn*4+3
+  const int tm = tid & 15;
+  const int tn = tid >> 4;
   float bd[8];
   int bi[8];
 #pragma unroll
@@ -198,7 +202,7 @@ k_assign_seq(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int
     __syncthreads();
     const int nc = min(kAsgBN, k - cb);
     for (int e = tid; e < kAsgBN * d; e += blockDim.x) {
-      const int j = e / d, t = e - j * d;
+      const int t = e / kAsgBN, j = e - t * kAsgBN;
       cs[t * kAsgPadN + j] = (j < nc) ? P.centers[(int64_t)(cb + j) * d + t] : 0.f;
     }
     for (int j = tid; j < kAsgBN; j += blockDim.x) s_cc[j] = (j < nc) ? P.cc[cb + j] : 0.f;
@@ -209,12 +213,12 @@ k_assign_seq(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-      const float* xp = xs + tm * 8;
+      const float* xp = xs + tm * 4;
       const float* cp = cs + tn * 4;
 #pragma unroll 4
       for (int t = 0; t < d; ++t) {
         const float4 a0 = *reinterpret_cast<const float4*>(xp + t * kAsgPadM);
-        const float4 a1 = *reinterpret_cast<const float4*>(xp + t * kAsgPadM + 4);
+        const float4 a1 = *reinterpret_cast<const float4*>(xp + t * kAsgPadM + 64);
         const float4 b = *reinterpret_cast<const float4*>(cp + t * kAsgPadN);
         const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
         const float bb[4] = {b.x, b.y, b.z, b.w};
@@ -225,7 +229,8 @@ k_assign_seq(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float xx = s_xx[tm * 8 + i];
+        const int rr = (i < 4) ? tm * 4 + i : 64 + tm * 4 + (i - 4);
+        const float xx = s_xx[rr];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int jj = tn * 4 + j;
@@ -249,8 +254,9 @@ k_assign_seq(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int
   if (lane < 16) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      s_bd[warp * kAsgBM + tm * 8 + i] = bd[i];
-      s_bi[warp * kAsgBM + tm * 8 + i] = bi[i];
+      const int rr = (i < 4) ? tm * 4 + i : 64 + tm * 4 + (i - 4);
+      s_bd[warp * kAsgBM + rr] = bd[i];
+      s_bi[warp * kAsgBM + rr] = bi[i];
     }
   }
   const bool count = !(flags & AC_ASSIGN_MERGE);

@@ -327,12 +327,11 @@ def run_denoise_steps(step_inputs, params: PipelineParams | None = None, seed: i
         mse_layer.append(float(np.mean([float(m) for m in mses])))
         flagged.append(any(m.flag_full for m in plan.key_models))
 
-    n_forced = math.ceil(params.full_layer_quota * n_layers) if params.full_layer_quota > 0 else 0
-    forced = set(sorted(range(n_layers), key=lambda l: (-mse_layer[l], l))[:n_forced])
+    from .sharding import decide_policies
+    modes = decide_policies(mse_layer, flagged, params.full_layer_quota)
     policies = []
     for l in range(n_layers):
-        full = flagged[l] or l in forced
-        policies.append(LayerPolicy(mode="full" if full else "sparse",
+        policies.append(LayerPolicy(mode=modes[l],
                                     key_cluster_count=[m.k for m in plans[l].key_models],
                                     tau=list(plans[l].taus), topk=params.topk,
                                     q_clusters=params.q_clusters))
@@ -402,7 +401,9 @@ class LayerSession:
     reference's per-layer rule with quota 0); later steps warm-start."""
 
     def __init__(self, params: PipelineParams | None = None, seed: int = 0, layer: int = 0,
-                 out_dtype=None, attn_impl: str = "auto", head_offset: int = 0):
+                 out_dtype=None, attn_impl: str = "auto", head_offset: int = 0,
+                 reduce_flag=None):
+        self.reduce_flag = reduce_flag or (lambda local: local)
         self.params = params or PipelineParams()
         self.params.validate()
         self.seed, self.layer, self.head_offset = seed, layer, head_offset
@@ -425,7 +426,8 @@ class LayerSession:
         if self.t == 0:
             seeds = [self.seed + 7919 * self.layer + self.head_offset + h for h in range(H)]
             plan = run.plan(Q, K, seeds)
-            self.mode = "full" if any(m.flag_full for m in plan.key_models) else "sparse"
+            flagged = self.reduce_flag(any(m.flag_full for m in plan.key_models))
+            self.mode = "full" if flagged else "sparse"
             if self.mode == "sparse":
                 so = run.sparse(Q, K, V, plan.q_models, plan.reps, plan.key_models,
                                 self.params.topk)
