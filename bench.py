@@ -15,10 +15,11 @@ Multi-GPU: heads are sharded in contiguous blocks over ranks (no cross-head
 communication); the per-head outputs are all-gathered over NCCL inside the
 timed region.  Time is the max over ranks.
 
-``--impl reference`` times the reference's CPU implementation of the path
-(the bit-exact C/numpy port in oracle/, since the reference package itself
-is not installable on the GPU box) on the host cores: one head's warm step
-(a bounded sample) extrapolated to the layer.
+``--impl reference`` times the reference's own CPU implementation of the
+path — the unmodified ``adacluster`` package installed in baseline/_ref, run
+through its public ``adacluster_attention`` with all host threads (the
+bit-exact oracle port in oracle/ only if that install is missing): head 0's
+warm steps (a bounded sample) extrapolated to the layer.
 """
 
 from __future__ import annotations
@@ -146,43 +147,81 @@ def bf16_host(a):
     return torch.from_numpy(a).bfloat16().float().numpy()
 
 
+def _reference_pkg():
+    """The UNMODIFIED reference package installed into baseline/_ref
+    (pip install --no-index --no-build-isolation --no-deps --target baseline/_ref,
+    see DESIGN.md), or None when it is not installed."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "adacluster" / "__init__.py").exists():
+        return None
+    sys.path.insert(0, str(ref))
+    import adacluster
+    return adacluster
+
+
 def run_reference(args, cfg, rank):
+    """Reference arm: the reference's own CPU implementation of the path on
+    the host cores (all threads), through its public API
+    (adacluster_attention, pipeline.py:237).  Bounded sample: head 0's warm
+    denoising steps, extrapolated over the layer's heads."""
     if rank != 0:
         return
-    from oracle import oracle as O
+    R = _reference_pkg()
     steps = gen_head(cfg, 0)
     if cfg["dtype"] == "bf16":
         steps = [[tuple(bf16_host(a) for a in steps[t][0])] for t in range(2)]
     (q0, k0, v0), (q1, k1, v1) = steps[0][0], steps[1][0]
-    p = O.Params(q_clusters=65, topk=25, m0=100, n_max=1000, full_layer_quota=0.0)
-    st = O.HeadState()
-    t0 = time.perf_counter()
-    O.head_step(q0, k0, v0, None, st, 0, p)
-    cold = time.perf_counter() - t0
-    times = []
     inputs = [(q1, k1, v1), (q0, k0, v0)]
-    for i in range(args.warmup + args.steps):
-        q, k, v = inputs[i % 2]
+    times = []
+    if R is not None:
+        from threadpoolctl import threadpool_limits
+        cores = os.cpu_count() or 1
+        kind = "reference"
+        with threadpool_limits(cores):
+            p = R.PipelineParams(q_clusters=65, topk=25, m0=100, n_max=1000, full_layer_quota=0.0)
+            pol, st = R.LayerPolicy(topk=25), R.StepState()
+            t0 = time.perf_counter()
+            R.adacluster_attention(q0, k0, v0, pol, st, 0, p)
+            cold = time.perf_counter() - t0
+            for i in range(args.warmup + args.steps):
+                q, k, v = inputs[i % 2]
+                t0 = time.perf_counter()
+                R.adacluster_attention(q, k, v, pol, st, 0, p)
+                dt = time.perf_counter() - t0
+                if i >= args.warmup:
+                    times.append(dt)
+    else:  # reference not installed: the bit-exact oracle port
+        from oracle import oracle as O
+        kind = "port"
+        cores = cpu_threads()
+        p = O.Params(q_clusters=65, topk=25, m0=100, n_max=1000, full_layer_quota=0.0)
+        st = O.HeadState()
         t0 = time.perf_counter()
-        O.head_step(q, k, v, "sparse", st, 0, p)
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            times.append(dt)
+        O.head_step(q0, k0, v0, None, st, 0, p)
+        cold = time.perf_counter() - t0
+        for i in range(args.warmup + args.steps):
+            q, k, v = inputs[i % 2]
+            t0 = time.perf_counter()
+            O.head_step(q, k, v, "sparse", st, 0, p)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
     head_s = statistics.mean(times)
     layer_s = head_s * cfg["heads"]
     value = cfg["seq"] / layer_s
-    cores = cpu_threads()
     out = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": layer_s * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 (bf16-valued inputs)", "data": "synthetic",
+        "dtype": "f32 (bf16-valued inputs)" if cfg["dtype"] == "bf16" else "f32",
+        "data": "synthetic (reference generator, criterion-7 spec, per-head seed 1000+h)",
         "impl": "reference",
         "config": config_block(cfg, args.gpus),
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": f"1 of {cfg['heads']} heads, warm step at L={cfg['seq']}, "
-                                   f"mean of {args.steps} steps, x{cfg['heads']} extrapolated; "
-                                   f"cold step-0 plan {cold:.1f}s/head"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind,
+                         "sample": f"head 0 of {cfg['heads']}, warm step at L={cfg['seq']}, "
+                                   f"mean of {args.steps} steps ({head_s:.2f}s/head), "
+                                   f"x{cfg['heads']} extrapolated; cold step-0 plan "
+                                   f"{cold:.1f}s/head"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "cold_step_ms": cold * cfg["heads"] * 1e3,
     }
@@ -195,7 +234,7 @@ def config_block(cfg, n):
             "heads": cfg["heads"], "seq_len": cfg["seq"], "head_dim": cfg["dim"],
             "q_clusters": 65, "topk": 25, "drift_sigma": DRIFT,
             "parallelism": f"head-sharded x{n} + NCCL all-gather of outputs",
-            "l2_policy": "inputs larger than L2 (806 MB of Q/K/V per step, alternating step inputs)"}
+            "l2_policy": f"inputs larger than L2 ({3 * cfg['heads'] * cfg['seq'] * cfg['dim'] * (2 if cfg['dtype'] == 'bf16' else 4) / 1e6:.0f} MB of Q/K/V per step, alternating step inputs)"}
 
 
 # ---------------------------------------------------------------------------
