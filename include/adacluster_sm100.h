@@ -100,6 +100,7 @@ typedef struct ac_cluster_problem {
 #define AC_ST_FLAGS 3
 #define AC_ST_KPP_STOP 4
 #define AC_ST_REPAIRS 5
+#define AC_ST_FIXUPS 6   /* rows the tensor-core assign resolved with > 1 exact chain */
 
 /* ---- library ---------------------------------------------------------- */
 const char* ac_last_error(void);
@@ -154,10 +155,25 @@ int ac_lloyd_prepare(const ac_cluster_problem* probs, int nprob, int dtype,
                      int d, int64_t max_n, int max_k, void* stream);
 int ac_assign(const ac_cluster_problem* probs, int nprob, int dtype, int d,
               int64_t max_n, int max_k, int c_lo, int flags, void* stream);
-/* same with an explicit accumulation order (AC_ORDER_*) for the batch      */
+/* same with an explicit accumulation order (AC_ORDER_*) for the batch.
+ * host_probs (optional, HOST copy of `probs`): when given and the batch is
+ * eligible (d = 64, AC_ORDER_SEQ, k - c_lo <= 128, 16-byte aligned rows) the
+ * cross term runs on the tcgen05 tensor cores (k_assign_tc: 3-way bf16 split,
+ * TMA-fed, exact FMA-chain fix-up of near-ties in the epilogue); results are
+ * bit-identical to the all-FFMA kernel.                                      */
 int ac_assign_ordered(const ac_cluster_problem* probs, int nprob, int dtype,
                       int d, int64_t max_n, int max_k, int c_lo, int flags,
-                      int order, void* stream);
+                      int order, const ac_cluster_problem* host_probs,
+                      void* stream);
+
+/* assignment kernel selection (process-wide): AUTO = tensor cores when the
+ * batch is eligible, EXACT = always the all-FFMA sequential-chain kernel
+ * (the parity reference), TC = tensor cores or AC_ERR_PARAM.               */
+#define AC_ASSIGN_MODE_AUTO 0
+#define AC_ASSIGN_MODE_EXACT 1
+#define AC_ASSIGN_MODE_TC 2
+int ac_set_assign_mode(int mode);
+int ac_get_assign_mode(void);
 int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dtype,
                    int d, int64_t max_n, int max_k, int iter, int flags,
                    void* stream);

@@ -23,7 +23,8 @@ DTYPE_F32, DTYPE_BF16 = 0, 1
 ORDER_SEQ, ORDER_LANES16, ORDER_GEMV8 = 0, 1, 2
 SCORERS = {"quest": 0, "mean": 1, "clamped": 2, "given": 3}
 ASSIGN_MERGE, ASSIGN_ALL = 1, 2
-ST_ACTIVE, ST_NITER, ST_DONE, ST_FLAGS, ST_KPP_STOP, ST_REPAIRS = range(6)
+ST_ACTIVE, ST_NITER, ST_DONE, ST_FLAGS, ST_KPP_STOP, ST_REPAIRS, ST_FIXUPS = range(7)
+ASSIGN_MODE_AUTO, ASSIGN_MODE_EXACT, ASSIGN_MODE_TC = range(3)
 STATUS_WORDS = 8
 
 # struct layouts (must match the header; checked in tests/test_abi.py)
@@ -63,7 +64,9 @@ _SIGS = {
     "ac_lloyd": [_P, _I, _I, _I, _I64, _I, _I, _D, _I, _P, _P],
     "ac_lloyd_prepare": [_P, _I, _I, _I, _I64, _I, _P],
     "ac_assign": [_P, _I, _I, _I, _I64, _I, _I, _I, _P],
-    "ac_assign_ordered": [_P, _I, _I, _I, _I64, _I, _I, _I, _I, _P],
+    "ac_assign_ordered": [_P, _I, _I, _I, _I64, _I, _I, _I, _I, _P, _P],
+    "ac_set_assign_mode": [_I],
+    "ac_get_assign_mode": [],
     "ac_repair_sort": [_P, _I, _I, _I, _I64, _I, _I, _I, _P],
     "ac_segment_mean": [_P, _I, _I, _I, _I, _P, _P],
     "ac_sort_by_label": [_P, _I, _I64, _I, _P],

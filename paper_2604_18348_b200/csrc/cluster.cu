@@ -15,12 +15,6 @@
 
 namespace ac {
 
-// ---------------------------------------------------------------------------
-// numpy elementwise semantics that differ from the CUDA intrinsics on
-// signed zeros: np.maximum(a, b) = (a >= b || isnan(a)) ? a : b
-// ---------------------------------------------------------------------------
-AC_DEV float np_maximum(float a, float b) { return (a >= b || isnan(a)) ? a : b; }
-AC_DEV float np_minimum(float a, float b) { return (a <= b || isnan(a)) ? a : b; }
 
 // f32 NT dot product in the accumulation order of the reference's sgemm.
 template <typename GetX, typename GetC>
@@ -58,11 +52,6 @@ AC_DEV float ordered_dot(const GetX& gx, const GetC& gc, int d, int order, bool 
   return acc;
 }
 
-// d = (xx - 2 xc) + cc, clipped at 0 exactly as np.maximum(d, 0.0)
-AC_DEV float sq_dist(float xx, float xc, float cc) {
-  float d = __fadd_rn(__fsub_rn(xx, __fmul_rn(2.f, xc)), cc);
-  return np_maximum(d, 0.f);
-}
 
 // ---------------------------------------------------------------------------
 // K1: row squared norms and l2 normalisation (tensorops.py:59-76)
@@ -141,6 +130,7 @@ __global__ void k_status_init(const ac_cluster_problem* __restrict__ probs, int 
   st[AC_ST_FLAGS] = 0;
   st[AC_ST_KPP_STOP] = -1;
   st[AC_ST_REPAIRS] = 0;
+  st[AC_ST_FIXUPS] = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -919,7 +909,15 @@ __global__ void k_envelopes(const ac_cluster_problem* __restrict__ probs, int dt
 // ===========================================================================
 using namespace ac;
 
+namespace ac_host {
+bool assign_tc_eligible(const ac_cluster_problem* host_probs, int nprob, int dtype, int d,
+                        int c_lo, int order);
+int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* host_probs,
+                     int nprob, int dtype, int c_lo, int flags, cudaStream_t st);
+}  // namespace ac_host
+
 namespace {
+int g_assign_mode = AC_ASSIGN_MODE_AUTO;
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int set_smem(const void* fn, size_t bytes) {
@@ -970,8 +968,20 @@ extern "C" int ac_lloyd_prepare(const ac_cluster_problem* probs, int nprob, int 
 // one accumulation order; the host splits batches otherwise).
 static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
                        int64_t max_n, int max_k, int c_lo, int flags, int order,
-                       cudaStream_t st) {
+                       const ac_cluster_problem* host_probs, cudaStream_t st) {
   const unsigned tiles = (unsigned)((max_n + kAsgBM - 1) / kAsgBM);
+  const int mode = g_assign_mode;
+  const bool tc_ok = ac_host::assign_tc_eligible(host_probs, nprob, dtype, d, c_lo, order);
+  if (mode == AC_ASSIGN_MODE_TC && !tc_ok) {
+    ac_host::set_error("assign: tensor-core path forced but the batch is not eligible "
+                       "(needs D=64, general order, k-c_lo<=128, host descriptors)");
+    return AC_ERR_PARAM;
+  }
+  if (tc_ok && mode != AC_ASSIGN_MODE_EXACT) {
+    k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
+    AC_CHECK_LAUNCH("k_center_sqnorm");
+    return ac_host::assign_tc_launch(probs, host_probs, nprob, dtype, c_lo, flags, st);
+  }
   if (order == AC_ORDER_SEQ) {
     const size_t smem = assign_smem_bytes(d, max_k);
     int rc = set_smem((const void*)k_assign_seq, smem);
@@ -991,16 +1001,28 @@ static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
 
 extern "C" int ac_assign_ordered(const ac_cluster_problem* probs, int nprob, int dtype, int d,
                                  int64_t max_n, int max_k, int c_lo, int flags, int order,
-                                 void* stream) {
+                                 const ac_cluster_problem* host_probs, void* stream) {
   if (nprob <= 0 || max_n <= 0) return AC_OK;
   if (d < 1 || d > 256) { ac_host::set_error("assign: d=%d unsupported (1..256)", d); return AC_ERR_DIM; }
-  return assign_impl(probs, nprob, dtype, d, max_n, max_k, c_lo, flags, order, S(stream));
+  return assign_impl(probs, nprob, dtype, d, max_n, max_k, c_lo, flags, order, host_probs,
+                     S(stream));
 }
 
 extern "C" int ac_assign(const ac_cluster_problem* probs, int nprob, int dtype, int d,
                          int64_t max_n, int max_k, int c_lo, int flags, void* stream) {
-  return ac_assign_ordered(probs, nprob, dtype, d, max_n, max_k, c_lo, flags, AC_ORDER_SEQ, stream);
+  return ac_assign_ordered(probs, nprob, dtype, d, max_n, max_k, c_lo, flags, AC_ORDER_SEQ,
+                           nullptr, stream);
 }
+
+extern "C" int ac_set_assign_mode(int mode) {
+  if (mode < AC_ASSIGN_MODE_AUTO || mode > AC_ASSIGN_MODE_TC) {
+    ac_host::set_error("ac_set_assign_mode: bad mode %d", mode);
+    return AC_ERR_PARAM;
+  }
+  g_assign_mode = mode;
+  return AC_OK;
+}
+extern "C" int ac_get_assign_mode(void) { return g_assign_mode; }
 
 static int repair_sort_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
                             int64_t max_n, int max_k, int iter, int flags, cudaStream_t st) {
@@ -1053,7 +1075,7 @@ extern "C" int ac_lloyd(const ac_cluster_problem* probs, int nprob, int dtype, i
   int32_t* pinned = nullptr;
   if (poll_every > 0 && host_probs) cudaMallocHost(&pinned, sizeof(int32_t) * nprob);
   for (int it = 0; it < max_iter; ++it) {
-    if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, 0, order, st))) break;
+    if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, 0, order, host_probs, st))) break;
     if ((rc = repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, it, 0, st))) break;
     if ((rc = update_impl(probs, nprob, dtype, d, max_k, tol, 0, nullptr, st))) break;
     if (pinned && (it + 1) % poll_every == 0 && it + 1 < max_iter) {
@@ -1068,7 +1090,9 @@ extern "C" int ac_lloyd(const ac_cluster_problem* probs, int nprob, int dtype, i
   }
   if (pinned) cudaFreeHost(pinned);
   if (rc) return rc;
-  if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, AC_ASSIGN_ALL, order, st))) return rc;
+  if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, AC_ASSIGN_ALL, order, host_probs,
+                        st)))
+    return rc;
   return repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, -1, AC_ASSIGN_ALL, st);
 }
 

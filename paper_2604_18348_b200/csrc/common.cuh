@@ -77,6 +77,18 @@ AC_DEV T pw_sum(const Get& get, int n) {
   return pw_sum_rec<T>(get, 0, n);
 }
 
+// numpy elementwise semantics that differ from the CUDA intrinsics on
+// signed zeros: np.maximum(a, b) = (a >= b || isnan(a)) ? a : b
+AC_DEV float np_maximum(float a, float b) { return (a >= b || isnan(a)) ? a : b; }
+AC_DEV float np_minimum(float a, float b) { return (a <= b || isnan(a)) ? a : b; }
+
+// d = (xx - 2 xc) + cc, clipped at 0 exactly as np.maximum(d, 0.0)
+// (clustering.py:70-75); explicit intrinsics, never contracted
+AC_DEV float sq_dist(float xx, float xc, float cc) {
+  float d = __fadd_rn(__fsub_rn(xx, __fmul_rn(2.f, xc)), cc);
+  return np_maximum(d, 0.f);
+}
+
 AC_DEV float warp_min_f(float v) {
   for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;

@@ -181,7 +181,7 @@ class Batch:
 
     def assign(self, c_lo: int = 0, flags: int = L.ASSIGN_ALL):
         L.call("ac_assign_ordered", *self.args(), int(c_lo), int(flags), self.orders[0],
-               L.stream_ptr())
+               self.desc.ctypes.data, L.stream_ptr())
 
     def sort(self):
         """tile histograms must be current (written by assign)."""

@@ -1,0 +1,126 @@
+"""Tensor-core assignment (k_assign_tc) vs the all-FFMA exact kernel.
+
+The tcgen05 kernel computes x·c with a 3-way bf16 split and re-derives every
+near-tie candidate with the reference's exact sequential FMA chain, so its
+labels, winning distances and per-tile histograms must equal the exact
+kernel's bit for bit (which in turn equals the oracle — test_gpu_parity.py).
+Includes adversarial near-ties: duplicated centres and points equidistant
+from two centres.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(xs, centers, mode, c_lo=0, merge_from=None):
+    from paper_2604_18348_b200 import _lib as L
+    from paper_2604_18348_b200 import engine as E
+    ks = [int(c.shape[0]) for c in centers]
+    b = E.Batch(xs, ks, 1)
+    for p, c in enumerate(centers):
+        b.centers_of(p).copy_(c)
+    b.prepare()
+    flags = L.ASSIGN_ALL
+    if merge_from is not None:
+        b.labels.copy_(merge_from[0])
+        b.best.copy_(merge_from[1])
+        flags |= L.ASSIGN_MERGE
+    L.call("ac_set_assign_mode", mode)
+    try:
+        b.assign(c_lo, flags)
+    finally:
+        L.call("ac_set_assign_mode", L.ASSIGN_MODE_AUTO)
+    torch.cuda.synchronize()
+    return (b.labels.clone(), b.best.clone(), b.tile_hist.clone(),
+            b.status.view(b.P, L.STATUS_WORDS)[:, L.ST_FIXUPS].clone())
+
+
+def _compare(xs, centers, c_lo=0, merge_from=None):
+    from paper_2604_18348_b200 import _lib as L
+    a = _run(xs, centers, L.ASSIGN_MODE_TC, c_lo, merge_from)
+    e = _run(xs, centers, L.ASSIGN_MODE_EXACT, c_lo, merge_from)
+    assert torch.equal(a[0], e[0]), f"labels differ in {(a[0] != e[0]).sum().item()} rows"
+    assert torch.equal(a[1].view(torch.int32), e[1].view(torch.int32)), "best distances differ"
+    if merge_from is None:
+        assert torch.equal(a[2], e[2]), "tile histograms differ"
+    return a[3].cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n,k", [(200, 16), (127, 16), (128, 65), (129, 100), (5000, 128),
+                                 (70000, 65), (70000, 100)])
+def test_tc_assign_random(gpu, dtype, n, k):
+    g = torch.Generator().manual_seed(n * 131 + k)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    x = (torch.randn(n, 64, generator=g) * 20).to(tdt).cuda()
+    idx = torch.randint(0, n, (k,), generator=g)
+    c = (x.float().cpu()[idx] + torch.randn(k, 64, generator=g) * 0.5).cuda()
+    _compare([x], [c])
+
+
+def test_tc_assign_normalised_queries_batch(gpu):
+    """Unit-norm f32 rows (the query side), several heads per launch."""
+    g = torch.Generator().manual_seed(7)
+    xs, cs = [], []
+    for h in range(5):
+        n = 3000 + 977 * h
+        x = torch.randn(n, 64, generator=g)
+        x = (x / x.norm(dim=1, keepdim=True)).cuda()
+        c = x[torch.randint(0, n, (65,), generator=g).cuda()] * 0.9
+        xs.append(x.contiguous())
+        cs.append(c.contiguous())
+    fix = _compare(xs, cs)
+    assert (fix >= 0).all()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_tc_assign_exact_ties(gpu, dtype):
+    """Duplicated centres and rows exactly between two centres: the first
+    index must win, exactly as numpy's argmin."""
+    g = torch.Generator().manual_seed(3)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    base = torch.randn(40, 64, generator=g) * 10
+    c = torch.cat([base, base[:10], base[5:15]])           # 60 centres, 20 duplicated
+    mid = 0.5 * (base[:20] + base[20:40])                   # equidistant from pairs
+    pts = torch.cat([mid.repeat(30, 1), base.repeat(20, 1),
+                     torch.randn(2000, 64, generator=g) * 10])
+    x = pts.to(tdt).cuda().contiguous()
+    fix = _compare([x], [c.cuda()])
+    assert fix[0] > 0  # the duplicates must have gone through the exact fix-up
+
+
+def test_tc_assign_degenerate_rows(gpu):
+    """All-zero rows are equidistant from every centre (many candidates)."""
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(1000, 64, generator=g)
+    x[::7] = 0
+    c = torch.randn(100, 64, generator=g)
+    _compare([x.cuda()], [c.cuda()])
+
+
+def test_tc_assign_merge(gpu):
+    """Running multi-stage assignment: merge new centres [c_lo, k) into the
+    existing (label, best) with strict '<' (earlier centres win ties)."""
+    from paper_2604_18348_b200 import _lib as L
+    g = torch.Generator().manual_seed(11)
+    x = (torch.randn(9000, 64, generator=g) * 30).bfloat16().cuda()
+    c_old = torch.randn(100, 64, generator=g) * 30
+    c_new = torch.cat([c_old[:7], torch.randn(93, 64, generator=g) * 30])  # 7 exact duplicates
+    both = torch.cat([c_old, c_new]).cuda()
+    lab, best, _, _ = _run([x], [both[:100].contiguous()], L.ASSIGN_MODE_EXACT)
+    _compare([x], [both.contiguous()], c_lo=100, merge_from=(lab, best))
+
+
+def test_tc_assign_lloyd_parity(gpu, oracle):
+    """A full Lloyd run through the tensor-core path equals the oracle."""
+    rng = np.random.default_rng(1)
+    x = (rng.normal(size=(20000, 64)) * 5).astype(np.float32)
+    a = gpu.kmeans(x, 100, seed=4)
+    b = oracle.kmeans(x, 100, 4)
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centers, b.centers)
+    assert a.n_iter == b.n_iter
+    assert list(a.inertia_history) == list(b.inertia_history)
