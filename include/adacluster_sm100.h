@@ -101,6 +101,7 @@ typedef struct ac_cluster_problem {
 #define AC_ST_KPP_STOP 4
 #define AC_ST_REPAIRS 5
 #define AC_ST_FIXUPS 6   /* rows the tensor-core assign resolved with > 1 exact chain */
+#define AC_ST_WIDE 7     /* ... of which had > 2 candidates (exact over every centre)  */
 
 /* ---- library ---------------------------------------------------------- */
 const char* ac_last_error(void);

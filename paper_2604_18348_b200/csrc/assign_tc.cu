@@ -52,25 +52,25 @@ constexpr int BM = 128;     // rows per tile (== kAsgBM: shared tiling with the 
 constexpr int DIM = 64;     // head_dim handled by this kernel
 constexpr int NBMAX = 128;  // centres per problem per launch (k - c_lo)
 constexpr int MAXP = 32;    // problems per launch (tensor maps travel as kernel params)
-constexpr int XS_F32 = 2;   // f32 x stages
-constexpr int XS_BF16 = 4;  // bf16 x stages (the f32 plane region is free in bf16 mode)
 constexpr int THREADS = 448;
 constexpr int W_TMA = 0, W_MMA = 1, W_CONV0 = 2, W_EPI0 = 6;
-
 constexpr int XF_BYTES = BM * DIM * 4;  // f32 tile: two 16 KB SW128 boxes of 32 columns
 constexpr int PL_BYTES = BM * DIM * 2;  // one bf16 plane of a tile (16 KB)
-constexpr int CP_BYTES = NBMAX * DIM * 2;
-constexpr int OFF_X = 0;                              // f32: [2] x 32 KB | bf16: [4] x 16 KB
-constexpr int OFF_XP = OFF_X + XS_F32 * XF_BYTES;     // f32: [2][3] planes
-constexpr int OFF_CP = OFF_XP + XS_F32 * 3 * PL_BYTES;  // [3] centre planes
-constexpr int OFF_CC = OFF_CP + 3 * CP_BYTES;           // [NBMAX] ||c||^2
-constexpr int OFF_HIST = OFF_CC + NBMAX * 4;            // [2][NBMAX] label histograms
-constexpr int OFF_BAR = OFF_HIST + 2 * NBMAX * 4;
-constexpr int NBAR = 2 * XS_BF16 + 2 * 2 + 2 * 2;
-constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
-constexpr int SMEM = OFF_MISC + 64 + 1024;  // + 1 KB alignment slack
-static_assert(XS_BF16 * PL_BYTES <= OFF_CP - OFF_X, "bf16 ring must fit the x region");
-static_assert(SMEM <= 227 * 1024, "shared memory budget");
+constexpr int CF_STRIDE = DIM + 4;      // f32 centre rows, padded against bank conflicts
+constexpr int NBAR = 16;
+constexpr int QCAP = 64;  // per-warp queue of extra (row, centre) fix-up candidates
+constexpr int SMEM_MAX = 227 * 1024;
+
+// Shared-memory layout, sized per launch from the largest centre count
+// (cap = max round16(k - c_lo)).  f32 points: x stages (1 or 2) of 32 KB +
+// 2 x 3 split planes; bf16 points: 4 x 16 KB x stages (the MMA operand).
+// Then the centre planes [3][cap][64] bf16 (SW128), the exact f32 centres
+// [cap][68], ||c||^2 [128], two label histograms [2][128], the epilogue
+// warps' fix-up queues [8][64] x (entry, result), barriers.
+struct Layout {
+  int xs, xstride, off_xp, off_cp, cp_bytes, off_cf, off_cc, off_hist, off_q, off_bar, off_misc,
+      smem;
+};
 
 struct Params {
   CUtensorMap x[MAXP];
@@ -79,10 +79,31 @@ struct Params {
   int dtype;
   int c_lo;
   int flags;
+  Layout lay;
 };
 
+__host__ __device__ inline Layout make_layout(int dtype, int cap) {
+  Layout l;
+  const bool f32 = dtype == AC_DTYPE_F32;
+  l.xs = f32 ? (cap <= 80 ? 2 : 1) : 4;
+  l.xstride = f32 ? XF_BYTES : PL_BYTES;
+  l.off_xp = l.xs * l.xstride;
+  l.off_cp = l.off_xp + (f32 ? 2 * 3 * PL_BYTES : 0);
+  l.cp_bytes = cap * 128;
+  l.off_cf = l.off_cp + 3 * l.cp_bytes;
+  l.off_cc = l.off_cf + cap * CF_STRIDE * 4;
+  l.off_hist = l.off_cc + NBMAX * 4;
+  l.off_q = l.off_hist + 2 * NBMAX * 4;
+  l.off_bar = l.off_q + 8 * QCAP * 8;
+  l.off_misc = l.off_bar + NBAR * 8;
+  l.smem = l.off_misc + 64 + 1024;  // + alignment slack
+  return l;
+}
+
+// 1 KB-aligned view of dynamic shared memory (offset arithmetic on the
+// shared pointer itself, so the compiler keeps shared-space accesses)
 AC_DEV unsigned char* align1024(unsigned char* p) {
-  return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 // byte offset of 16-byte chunk j of row r in a 128-byte-row SW128 tile
 AC_DEV int sw128(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
@@ -121,20 +142,35 @@ AC_DEV void join8(const uint4& h, const uint4& m, const uint4& l, float (&v)[8])
   }
 }
 
-// exact reference distance of this thread's row (xr) to smem centre c
-AC_DEV float exact_dist(const unsigned char* cp, int c, const float (&xr)[DIM], float xx, float cc) {
-  const unsigned char* cb = cp + c * 128;
+// the reference's d for row r of the x tile and f32 centre row cf:
+// sequential fmaf chain from 0 (OpenBLAS general path), then sq_dist.
+// x comes from shared memory: the three split planes (f32 points, joined
+// exactly) or the bf16 tile itself.
+AC_DEV float exact_dist(const unsigned char* xsm, bool f32in, int r, const float* cf, float xx,
+                        float cc) {
   float acc = 0.f;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const int off = (j ^ (c & 7)) << 4;
-    const uint4 h = *reinterpret_cast<const uint4*>(cb + off);
-    const uint4 m = *reinterpret_cast<const uint4*>(cb + CP_BYTES + off);
-    const uint4 l = *reinterpret_cast<const uint4*>(cb + 2 * CP_BYTES + off);
-    float cv[8];
-    join8(h, m, l, cv);
+    const int off = sw128(r, j);
+    float xv[8];
+    if (f32in) {
+      join8(*reinterpret_cast<const uint4*>(xsm + off),
+            *reinterpret_cast<const uint4*>(xsm + PL_BYTES + off),
+            *reinterpret_cast<const uint4*>(xsm + 2 * PL_BYTES + off), xv);
+    } else {
+      const uint4 w = *reinterpret_cast<const uint4*>(xsm + off);
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc = __fmaf_rn(xr[8 * j + e], cv[e], acc);
+      for (int e = 0; e < 4; ++e) {
+        xv[2 * e] = bf_lo(ww[e]);
+        xv[2 * e + 1] = bf_hi(ww[e]);
+      }
+    }
+    const float4 c0 = *reinterpret_cast<const float4*>(cf + 8 * j);
+    const float4 c1 = *reinterpret_cast<const float4*>(cf + 8 * j + 4);
+    const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc = __fmaf_rn(xv[e], cv[e], acc);
   }
   return sq_dist(xx, acc, cc);
 }
@@ -145,24 +181,26 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
   unsigned char* sm = align1024(smraw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool f32in = prm.dtype == AC_DTYPE_F32;
-  const int XS = f32in ? XS_F32 : XS_BF16;
-  const int XSTRIDE = f32in ? XF_BYTES : PL_BYTES;
+  const Layout& lay = prm.lay;
+  const int XS = lay.xs;
 
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
-  uint64_t* xfull = bars;
-  uint64_t* xempty = bars + XS_BF16;
-  uint64_t* pfull = bars + 2 * XS_BF16;
-  uint64_t* pempty = pfull + 2;
-  uint64_t* afull = pfull + 4;
-  uint64_t* aempty = pfull + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_MISC);
-  int* s_ccmax = reinterpret_cast<int*>(sm + OFF_MISC + 16);
-  float* s_cc = reinterpret_cast<float*>(sm + OFF_CC);
-  int* s_hist = reinterpret_cast<int*>(sm + OFF_HIST);
-  unsigned char* cplanes = sm + OFF_CP;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + lay.off_bar);
+  uint64_t* xfull = bars;       // [4] TMA -> converter (f32) / MMA (bf16)
+  uint64_t* xempty = bars + 4;  // [4] converter (f32) / epilogue (bf16) -> TMA
+  uint64_t* pfull = bars + 8;   // [2] converter -> MMA
+  uint64_t* pempty = bars + 10; // [2] epilogue -> converter
+  uint64_t* afull = bars + 12;  // [2] MMA commit -> epilogue
+  uint64_t* aempty = bars + 14; // [2] epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + lay.off_misc);
+  int* s_ccmax = reinterpret_cast<int*>(sm + lay.off_misc + 16);
+  float* s_cc = reinterpret_cast<float*>(sm + lay.off_cc);
+  int* s_hist = reinterpret_cast<int*>(sm + lay.off_hist);
+  unsigned char* cplanes = sm + lay.off_cp;
+  float* cf32 = reinterpret_cast<float*>(sm + lay.off_cf);
+  const int CPB = lay.cp_bytes;
 
   if (tid == 0) {
-    for (int s = 0; s < XS_BF16; ++s) {
+    for (int s = 0; s < 4; ++s) {
       mbar_init(xfull + s, 1);
       mbar_init(xempty + s, 128);
     }
@@ -201,7 +239,8 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
     const int ntiles_p = prm.tile0[p + 1] - ptile0;
     const int T = seg_end - t;
 
-    // ---- centre planes, ||c||^2 and max ||c||^2 of this problem (all threads) ----
+    // ---- centres of this problem: bf16 planes (MMA), exact f32 rows
+    //      (fix-up), ||c||^2 (+inf past nb, masking the pad columns) ----
     if (tid == 0) *s_ccmax = 0;
     __syncthreads();
     for (int e = tid; e < nbp * 8; e += THREADS) {
@@ -212,6 +251,9 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const float4 a = src[0], b = src[1];
         v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
         v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        float4* dst = reinterpret_cast<float4*>(cf32 + c * CF_STRIDE + 8 * j);
+        dst[0] = a;
+        dst[1] = b;
       } else {
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = 0.f;
@@ -220,11 +262,11 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       split8(v, h, m, l);
       const int off = sw128(c, j);
       *reinterpret_cast<uint4*>(cplanes + off) = h;
-      *reinterpret_cast<uint4*>(cplanes + CP_BYTES + off) = m;
-      *reinterpret_cast<uint4*>(cplanes + 2 * CP_BYTES + off) = l;
+      *reinterpret_cast<uint4*>(cplanes + CPB + off) = m;
+      *reinterpret_cast<uint4*>(cplanes + 2 * CPB + off) = l;
     }
-    for (int c = tid; c < nbp; c += THREADS) {
-      const float cc = (c < nb) ? P.cc[c_lo + c] : 0.f;
+    for (int c = tid; c < NBMAX; c += THREADS) {
+      const float cc = (c < nb) ? P.cc[c_lo + c] : INFINITY;
       s_cc[c] = cc;
       if (c < nb && cc > 0.f) atomicMax(s_ccmax, __float_as_int(cc));
     }
@@ -238,9 +280,9 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       if (lane == 0) {
         for (int i = 0; i < T; ++i) {
           const int g = g0 + i, s = g % XS;
-          if (g >= XS) mbar_wait(xempty + s, ((g / XS) - 1) & 1, 20);
+          if (g >= XS) mbar_wait_sleep(xempty + s, ((g / XS) - 1) & 1, 20);
           const int row = (t + i - ptile0) * BM;
-          unsigned char* dst = sm + OFF_X + s * XSTRIDE;
+          unsigned char* dst = sm + s * lay.xstride;
           if (f32in) {
             mbar_expect_tx(xfull + s, XF_BYTES);
             tma_load_2d(dst, &prm.x[p], 0, row, xfull + s);
@@ -257,24 +299,28 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       if (lane == 0) {
         const uint32_t idesc = idesc_bf16(BM, nbp, false);
         const uint32_t ca = smem_u32(cplanes);
-        // plane products kept: (x plane, c plane); dropped terms are < 2^-23 relative
-        const int xi[6] = {0, 0, 1, 0, 1, 2};
-        const int ci[6] = {0, 1, 0, 2, 1, 0};
+        // plane products kept: (x plane, c plane), the x-hi terms first (bf16
+        // points are exact in plane 0, so they use only those three); the
+        // dropped terms are < 2^-23 relative
+        const int xi[6] = {0, 0, 0, 1, 1, 2};
+        const int ci[6] = {0, 1, 2, 0, 1, 0};
         const int nterm = f32in ? 6 : 3;
         for (int i = 0; i < T; ++i) {
           const int g = g0 + i, s = g % XS, b = g & 1;
-          if (f32in) mbar_wait(pfull + b, (g >> 1) & 1, 21);
-          else mbar_wait(xfull + s, (g / XS) & 1, 22);
-          if (g >= 2) mbar_wait(aempty + b, ((g >> 1) - 1) & 1, 23);
+          if (f32in) mbar_wait_sleep(pfull + b, (g >> 1) & 1, 21);
+          else mbar_wait_sleep(xfull + s, (g / XS) & 1, 22);
+          if (g >= 2) mbar_wait_sleep(aempty + b, ((g >> 1) - 1) & 1, 23);
           fence_after();
-          const uint32_t xa = f32in ? smem_u32(sm + OFF_XP + b * 3 * PL_BYTES)
-                                    : smem_u32(sm + OFF_X + s * PL_BYTES);
+          const uint32_t xa = f32in ? smem_u32(sm + lay.off_xp + b * 3 * PL_BYTES)
+                                    : smem_u32(sm + s * PL_BYTES);
           const uint32_t d = tmem + (uint32_t)(b * 128);
-          for (int term = 0; term < nterm; ++term) {
+#pragma unroll
+          for (int term = 0; term < 6; ++term) {
+            if (term >= nterm) break;
 #pragma unroll
             for (int kk = 0; kk < DIM / 16; ++kk) {
               const uint64_t ad = sdesc(xa + xi[term] * PL_BYTES + kk * 32, 16, 1024);
-              const uint64_t bd = sdesc(ca + ci[term] * CP_BYTES + kk * 32, 16, 1024);
+              const uint64_t bd = sdesc(ca + ci[term] * CPB + kk * 32, 16, 1024);
               umma_f16(d, ad, bd, idesc, (term > 0 || kk > 0) ? 1u : 0u);
             }
           }
@@ -288,10 +334,10 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const int r = tid - W_CONV0 * 32;  // 0..127
         for (int i = 0; i < T; ++i) {
           const int g = g0 + i, s = g % XS, b = g & 1;
-          mbar_wait(xfull + s, (g / XS) & 1, 24);
-          if (g >= 2) mbar_wait(pempty + b, ((g >> 1) - 1) & 1, 25);
-          const unsigned char* xs = sm + OFF_X + s * XF_BYTES;
-          unsigned char* xp = sm + OFF_XP + b * 3 * PL_BYTES;
+          mbar_wait_sleep(xfull + s, (g / XS) & 1, 24);
+          if (g >= 2) mbar_wait_sleep(pempty + b, ((g >> 1) - 1) & 1, 25);
+          const unsigned char* xs = sm + s * XF_BYTES;
+          unsigned char* xp = sm + lay.off_xp + b * 3 * PL_BYTES;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const unsigned char* box = xs + (j >> 2) * (XF_BYTES / 2);
@@ -313,12 +359,14 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       }
     } else {
       // ------------------------------ epilogue ------------------------------
+      // e_c = cc - 2 acc ~ d~_c - ||x||^2; candidates: max(xx + e_c, 0) <=
+      // d~_min + 2T  <=>  e_c <= d~_min + 2T - xx (slack 0.5T for roundings)
       const int wg = (warp - W_EPI0) >> 2;
       const int q = warp & 3;  // TMEM lane quarter this warp may access
       const int r = q * 32 + lane;
       const uint32_t lane_base = (uint32_t)(q * 32) << 16;
       int* hist = s_hist + wg * NBMAX;
-      int fixups = 0;
+      int fixups = 0, wide = 0;
       for (int i = 0; i < T; ++i) {
         const int g = g0 + i;
         if ((g & 1) != wg) continue;
@@ -327,95 +375,108 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const int64_t row = (int64_t)tile * BM + r;
         const bool valid = row < n;
         const float xx = valid ? P.xx[row] : 0.f;
-        // rigorous bound on |d~ - d_ref|
-        const float tb = 0x1p-13f * sqrtf(xx) * cmax + 0x1p-20f * (xx + ccmax) + 1e-30f;
-        mbar_wait(afull + b, (g >> 1) & 1, 26);
+        const float tb = 0x1p-15f * sqrtf(xx) * cmax + 0x1p-20f * (xx + ccmax) + 1e-30f;
+        mbar_wait_sleep(afull + b, (g >> 1) & 1, 26);
         fence_after();
         const uint32_t acc_col = tmem + lane_base + (uint32_t)(b * 128);
-        float dmin = INFINITY;
+        float emin = INFINITY;
         for (int c0 = 0; c0 < nbp; c0 += 32) {
           uint32_t v[32];
           tmem_ld32(acc_col + c0, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            const int c = c0 + u;
-            if (c < nb) {
-              const float d = sq_dist(xx, __uint_as_float(v[u]), s_cc[c]);
-              if (d < dmin) dmin = d;
-            }
-          }
+          for (int u = 0; u < 32; ++u)
+            emin = fminf(emin, __fmaf_rn(-2.f, __uint_as_float(v[u]), s_cc[c0 + u]));
         }
-        const float thr = dmin + 2.f * tb;
-        int c1 = -1, c2 = -1, ncand = 0;
-        for (int c0 = 0; c0 < nbp; c0 += 32) {
+        const float dmin = fmaxf(xx + emin, 0.f);
+        const float ethr = (dmin + 2.5f * tb) - xx;
+        int c1 = INT_MAX, ncand = 0;
+        uint32_t mk[NBMAX / 32];
+#pragma unroll
+        for (int ch = 0; ch < NBMAX / 32; ++ch) {
+          mk[ch] = 0u;
+          const int c0 = ch * 32;
+          if (c0 >= nbp) continue;
           uint32_t v[32];
           tmem_ld32(acc_col + c0, v);
           tmem_wait_ld();
+          uint32_t m = 0;
 #pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            const int c = c0 + u;
-            if (c < nb) {
-              const float d = sq_dist(xx, __uint_as_float(v[u]), s_cc[c]);
-              if (d <= thr) {
-                c1 = (ncand == 0) ? c : c1;
-                c2 = (ncand == 1) ? c : c2;
-                ++ncand;
-              }
-            }
+          for (int u = 0; u < 32; ++u)
+            m |= (__fmaf_rn(-2.f, __uint_as_float(v[u]), s_cc[c0 + u]) <= ethr) ? (1u << u) : 0u;
+          mk[ch] = m;
+          if (m) {
+            c1 = min(c1, c0 + __ffs(m) - 1);
+            ncand += __popc(m);
           }
         }
         fence_before();
         mbar_arrive(aempty + b);
 
-        // this row's exact f32 values
-        float xr[DIM];
-        if (f32in) {
-          const unsigned char* xp = sm + OFF_XP + b * 3 * PL_BYTES;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int off = sw128(r, j);
-            float v8[8];
-            join8(*reinterpret_cast<const uint4*>(xp + off),
-                  *reinterpret_cast<const uint4*>(xp + PL_BYTES + off),
-                  *reinterpret_cast<const uint4*>(xp + 2 * PL_BYTES + off), v8);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) xr[8 * j + e] = v8[e];
-          }
-        } else {
-          const unsigned char* xb = sm + OFF_X + s * PL_BYTES;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint4 w = *reinterpret_cast<const uint4*>(xb + sw128(r, j));
-            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              xr[8 * j + 2 * e] = bf_lo(ww[e]);
-              xr[8 * j + 2 * e + 1] = bf_hi(ww[e]);
-            }
-          }
-        }
+        // exact chains: every row's first candidate on its own lane, then the
+        // warp's extra candidates (near-ties) spread over all 32 lanes
+        const unsigned char* xsm = f32in ? sm + lay.off_xp + b * 3 * PL_BYTES : sm + s * PL_BYTES;
         float best = INFINITY;
         int lbl = INT_MAX;
-        if (valid) {
-          if (ncand <= 2) {
-            if (ncand >= 1) {
-              const float d = exact_dist(cplanes, c1, xr, xx, s_cc[c1]);
-              if (d < best) { best = d; lbl = c1; }
+        if (valid && ncand >= 1) {
+          best = exact_dist(xsm, f32in, r, cf32 + c1 * CF_STRIDE, xx, s_cc[c1]);
+          lbl = c1;
+          if (!(best < INFINITY)) { best = INFINITY; lbl = INT_MAX; }  // as `d < best` from +inf
+        }
+        const int extra = (valid && ncand > 1) ? ncand - 1 : 0;
+        int incl = extra;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total > 0) {
+          uint32_t* qe = reinterpret_cast<uint32_t*>(sm + lay.off_q) + (warp - W_EPI0) * 2 * QCAP;
+          float* qr = reinterpret_cast<float*>(qe + QCAP);
+          const int off = incl - extra;
+          if (total <= QCAP) {
+            int e = off;
+#pragma unroll
+            for (int ch = 0; ch < NBMAX / 32; ++ch) {
+              uint32_t m = mk[ch];
+              while (m) {
+                const int c = ch * 32 + __ffs(m) - 1;
+                m &= m - 1;
+                if (c != c1) qe[e++] = ((uint32_t)lane << 8) | (uint32_t)c;
+              }
             }
-            if (ncand == 2) {
-              const float d = exact_dist(cplanes, c2, xr, xx, s_cc[c2]);
-              if (d < best) { best = d; lbl = c2; }
+            __syncwarp();
+            for (int e2 = lane; e2 < total; e2 += 32) {
+              const int src = (int)(qe[e2] >> 8), c = (int)(qe[e2] & 255u);
+              const int64_t srow = (int64_t)tile * BM + q * 32 + src;
+              qr[e2] = exact_dist(xsm, f32in, q * 32 + src, cf32 + c * CF_STRIDE, P.xx[srow], s_cc[c]);
             }
-          } else {  // many near-ties (degenerate rows): exact over every centre
-            for (int c = 0; c < nb; ++c) {
-              const float d = exact_dist(cplanes, c, xr, xx, s_cc[c]);
-              if (d < best) { best = d; lbl = c; }
+            __syncwarp();
+            for (int e2 = off; e2 < off + extra; ++e2) {  // ascending centre order
+              const float d = qr[e2];
+              if (d < best) { best = d; lbl = (int)(qe[e2] & 255u); }
+            }
+            __syncwarp();
+          } else {  // very many near-ties in this warp: each lane walks its own
+#pragma unroll
+            for (int ch = 0; ch < NBMAX / 32; ++ch) {
+              uint32_t m = mk[ch];
+              while (m) {
+                const int c = ch * 32 + __ffs(m) - 1;
+                m &= m - 1;
+                if (c == c1) continue;
+                const float d = exact_dist(xsm, f32in, r, cf32 + c * CF_STRIDE, xx, s_cc[c]);
+                if (d < best) { best = d; lbl = c; }
+              }
             }
           }
-          fixups += (ncand >= 2);
         }
-        // x values are no longer needed: release the stage / planes
+        if (valid) {
+          fixups += (ncand >= 2);
+          wide += (ncand > 2);
+        }
+        // x is no longer needed: release the planes / stage
         if (f32in) mbar_arrive(pempty + b);
         else mbar_arrive(xempty + s);
 
@@ -440,7 +501,9 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       }
       // per-problem statistics: rows that needed more than one exact chain
       fixups = __reduce_add_sync(0xffffffffu, fixups);
+      wide = __reduce_add_sync(0xffffffffu, wide);
       if (lane == 0 && fixups) atomicAdd(&P.status[AC_ST_FIXUPS], fixups);
+      if (lane == 0 && wide) atomicAdd(&P.status[AC_ST_WIDE], wide);
     }
     g0 += T;
     t = seg_end;
@@ -487,13 +550,21 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e = cudaFuncSetAttribute((const void*)k_assign_tc,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     if (e != cudaSuccess) return check_cuda(e, "k_assign_tc smem");
   }
   for (int p0 = 0; p0 < nprob; p0 += MAXP) {
     const int np = std::min(MAXP, nprob - p0);
     Params prm;
     memset(&prm, 0, sizeof(prm));
+    int cap = 16;
+    for (int j = 0; j < np; ++j)
+      cap = std::max(cap, (host_probs[p0 + j].k - c_lo + 15) & ~15);
+    prm.lay = make_layout(dtype, cap);
+    if (prm.lay.smem > SMEM_MAX) {
+      set_error("k_assign_tc: shared-memory layout %d B exceeds the budget", prm.lay.smem);
+      return AC_ERR_PARAM;
+    }
     prm.nprob = np;
     prm.dtype = dtype;
     prm.c_lo = c_lo;
@@ -515,7 +586,7 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     const int total = prm.tile0[np];
     if (total == 0) continue;
     const int grid = std::min(total, sms);
-    k_assign_tc<<<grid, THREADS, SMEM, st>>>(prm, probs + p0);
+    k_assign_tc<<<grid, THREADS, prm.lay.smem, st>>>(prm, probs + p0);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return check_cuda(e, "k_assign_tc");
   }

@@ -131,6 +131,7 @@ __global__ void k_status_init(const ac_cluster_problem* __restrict__ probs, int 
   st[AC_ST_KPP_STOP] = -1;
   st[AC_ST_REPAIRS] = 0;
   st[AC_ST_FIXUPS] = 0;
+  st[AC_ST_WIDE] = 0;
 }
 
 // ---------------------------------------------------------------------------

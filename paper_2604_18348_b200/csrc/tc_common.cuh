@@ -48,6 +48,31 @@ AC_DEV void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
   }
 }
 
+// try_wait with a suspend-time hint: the waiting thread sleeps until the
+// phase completes (or the hint expires) instead of spinning on the issue
+// slots that the working warps of the same SM sub-partition need
+AC_DEV bool mbar_try_wait_hint(uint32_t addr, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+AC_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, int tag = 0) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t spins = 0;
+  while (!mbar_try_wait_hint(a, parity, 0x10000u)) {
+    if (++spins == (1u << 16)) {
+      printf("tcgen05 kernel watchdog: block %d thread %d tag %d parity %u\n", blockIdx.x,
+             threadIdx.x, tag, parity);
+      asm volatile("trap;");
+    }
+  }
+}
+
 AC_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"

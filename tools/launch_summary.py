@@ -1,0 +1,19 @@
+"""Aggregate an ncu --metrics gpu__time_duration.sum launch list per kernel."""
+import collections, csv, sys
+rows = list(csv.reader(open(sys.argv[1])))
+h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+hdr = rows[h]
+ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+agg = collections.defaultdict(lambda: [0, 0.0])
+scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+for r in rows[h + 1:]:
+    if len(r) <= vi:
+        continue
+    v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-3)
+    name = r[ki].split("(")[0][:60]
+    agg[name][0] += 1
+    agg[name][1] += v
+tot = sum(t for _, t in agg.values())
+for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+    print(f"{t:9.3f} ms {100 * t / tot:5.1f}% {n:5d}  {k}")
+print(f"{tot:9.3f} ms total, {sum(n for n, _ in agg.values())} launches")
