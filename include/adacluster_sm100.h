@@ -273,7 +273,12 @@ int ac_build_q_layout(const void* q, int dtype, int d, int64_t L, int heads,
                       const int32_t* qcounts, const int32_t* qlabels,
                       const int32_t* gq, int gq_max, const int32_t* nruns,
                       int topk_max, void* qp, int32_t* qidx, int64_t qp_cap,
-                      ac_attn_item* items, int item_cap, void* stream);
+                      ac_attn_item* items, int item_cap, int item_rows,
+                      void* stream);
+/* rows per work item the attention kernel for (dtype, d) expects from
+ * ac_build_q_layout: 256 for the two-tile tcgen05 kernel (bf16, d = 64),
+ * else 128                                                                 */
+int ac_attention_item_rows(int dtype, int d);
 
 /* ---- K13/K14 block-sparse attention --------------------------------------
  * One work item = one tile of <= 128 query rows of one query cluster of one
@@ -285,8 +290,9 @@ int ac_build_q_layout(const void* q, int dtype, int d, int64_t L, int heads,
  * k/v: Kp/Vp [heads, L, d] (dtype), runs: [*, 2] int32 ranges into [0, L)
  * out: [heads, L, d] f32 or bf16 (out_dtype), written at original rows.
  * scale: softmax scale (1/sqrt(d) in the reference, reference.py:39).
- * bf16 inputs with d in {64, 128} run on the tcgen05 kernel; everything else
- * (f32 inputs: the 1e-4 parity bar needs f32 math) on the CUDA-core kernel. */
+ * bf16 inputs with d = 64 run on the two-Q-tile tcgen05 kernel (items of up to
+ * 256 rows), d = 128 on the one-tile tcgen05 kernel; everything else (f32
+ * inputs: the 1e-4 parity bar needs f32 math) on the CUDA-core kernel.     */
 int ac_sparse_attention(const void* q, int64_t q_rows_total, const int32_t* qidx,
                         const void* k, const void* v, int dtype, int d, int64_t L,
                         int heads, const ac_attn_item* items, int nitems,
@@ -298,6 +304,12 @@ int ac_sparse_attention_simt(const void* q, const int32_t* qidx, const void* k,
                              const ac_attn_item* items, int nitems,
                              const int32_t* runs, float scale, void* out,
                              int out_dtype, void* stream);
+int ac_sparse_attention_fa4(const void* q, int64_t q_rows_total,
+                            const int32_t* qidx, const void* k, const void* v,
+                            int d, int64_t L, int heads,
+                            const ac_attn_item* items, int nitems,
+                            const int32_t* runs, float scale, void* out,
+                            int out_dtype, void* stream);
 int ac_sparse_attention_tc(const void* q, int64_t q_rows_total,
                            const int32_t* qidx, const void* k, const void* v,
                            int d, int64_t L, int heads,

@@ -81,8 +81,10 @@ _SIGS = {
     "ac_permute_rows": [_P, _I, _I, _P, _I64, _P, _P],
     "ac_permute_rows_heads": [_P, _I, _I, _P, _I64, _I, _P, _P],
     "ac_build_q_layout": [_P, _I, _I, _I64, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P, _I64,
-                          _P, _I, _P],
+                          _P, _I, _I, _P],
+    "ac_attention_item_rows": [_I, _I],
     "ac_sparse_attention": [_P, _I64, _P, _P, _P, _I, _I, _I64, _I, _P, _I, _P, _F, _P, _I, _P],
+    "ac_sparse_attention_fa4": [_P, _I64, _P, _P, _P, _I, _I64, _I, _P, _I, _P, _F, _P, _I, _P],
     "ac_sparse_attention_tc": [_P, _I64, _P, _P, _P, _I, _I64, _I, _P, _I, _P, _F, _P, _I, _P],
     "ac_sparse_attention_simt": [_P, _P, _P, _P, _I, _I, _I64, _P, _I, _P, _F, _P, _I, _P],
 }

@@ -34,6 +34,7 @@ UNITS = {
     "select.cu": ["--fmad=false"],
     "attn_simt.cu": [],
     "attn_tc.cu": [],
+    "attn_fa4.cu": [],
     "assign_tc.cu": ["--fmad=false"],
 }
 

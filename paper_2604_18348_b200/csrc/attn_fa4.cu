@@ -1,0 +1,433 @@
+// Block-sparse flash attention for head_dim 64 on the 5th-generation tensor
+// cores, two query tiles per CTA (FA4-style ping-pong).
+//
+// Reference semantics: pipeline.py:154-165 (_gathered_attention) and
+// reference.py:25-45 (full_attention): every query cluster attends, with a
+// plain softmax (scale 1/sqrt(D), max-subtracted), over the union of its
+// selected key clusters.  Keys/values are stored cluster-contiguous (Kp/Vp),
+// so a query cluster's keys are a handful of [start, end) runs, walked in
+// 128-key tiles; keys past a run's end are masked.
+//
+// One CTA = one work item = up to 256 query rows (two 128-row tiles) of one
+// query cluster, which share every K/V tile:
+//   warps 0-3   softmax of Q tile 0 (thread = query row = TMEM lane)
+//   warps 4-7   softmax of Q tile 1
+//   warp 8      TMA producer: Q0/Q1 once, K/V tiles through a 4-stage ring
+//   warp 9      MMA issuer: S_t = Q_t·Kᵀ into TMEM (kind::f16, f32 accum),
+//               O_t += P_t·V with P_t read from TMEM (the A-from-TMEM form)
+// TMEM (512 columns): S0 | S1 (128 each) | O0 | O1 (64 each) | P0 | P1
+// (64 x 32-bit columns = 128 bf16 each).  While one tile's softmax runs the
+// tensor core works on the other tile's S or PV.
+// Softmax in the exp2 domain with lazy rescaling (the running max only
+// moves when a row max grows by more than 2^8); ~3/8 of the exponentials
+// are evaluated with a cubic polynomial on the FMA pipe (packed f32x2) to
+// offload the MUFU unit, which otherwise bounds D = 64 attention on B200.
+// Epilogue: O / l, bf16 or f32, stored at the query's original token row
+// (the inverse permutation is fused into the store).
+#include <cfloat>
+
+#include "tc_common.cuh"
+
+namespace ac {
+namespace fa {
+using namespace ac::tc;
+
+constexpr int D = 64;
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int STAGES = 4;
+constexpr int THREADS = 320;
+constexpr int W_TMA = 8, W_MMA = 9;
+constexpr int Q_BYTES = BM * D * 2;
+constexpr int KV_BYTES = BN * D * 2;
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
+constexpr int OFF_V = OFF_K + STAGES * KV_BYTES;
+constexpr int OFF_BAR = OFF_V + STAGES * KV_BYTES;
+constexpr int NBAR = 1 + 2 * STAGES + 2 + 2 + 2;
+constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
+constexpr int SMEM = OFF_MISC + 16 + 1024;
+constexpr uint32_t COL_S = 0, COL_O = 256, COL_P = 384;
+
+AC_DEV void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                    uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+AC_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+
+// packed f32x2 helpers (FFMA2 / FADD2 on sm_100)
+AC_DEV uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+AC_DEV void up2(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+AC_DEV uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+AC_DEV uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+AC_DEV uint64_t add2_rm(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^x for a pair on the FMA pipe: x = n + f, f in [0,1), 2^f by a cubic
+// (max rel. error 7.5e-5, below the bf16 rounding of P), n into the exponent
+AC_DEV void exp2_poly2(float x0, float x1, float& p0, float& p1) {
+  const float kMagic = 12582912.f;  // 1.5 * 2^23
+  // clamp so that the result exponent stays >= 1 (poly(f) >= 0.9999, n >= -125)
+  x0 = fmaxf(x0, -125.f);
+  x1 = fmaxf(x1, -125.f);
+  const uint64_t x = pk2(x0, x1);
+  const uint64_t xr = add2_rm(x, pk2(kMagic, kMagic));          // floor(x) in the low bits
+  const uint64_t nf = add2(xr, pk2(-kMagic, -kMagic));          // floor(x) as float
+  float n0, n1;
+  up2(nf, n0, n1);
+  const uint64_t f = add2(x, pk2(-n0, -n1));
+  uint64_t p = fma2(pk2(0.07802446f, 0.07802446f), f, pk2(0.22606731f, 0.22606731f));
+  p = fma2(p, f, pk2(0.69583344f, 0.69583344f));
+  p = fma2(p, f, pk2(0.99992523f, 0.99992523f));
+  float q0, q1, r0, r1;
+  up2(p, q0, q1);
+  up2(xr, r0, r1);
+  p0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(r0) << 23));
+  p1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(r1) << 23));
+}
+
+AC_DEV uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// the K/V tiles of one work item: its runs walked in BN-key steps
+struct TileIter {
+  const int32_t* runs;
+  int nruns, r, s, e;
+  AC_DEV TileIter(const int32_t* runs_, int nruns_) : runs(runs_), nruns(nruns_), r(-1), s(0), e(0) {}
+  AC_DEV bool next(int& start, int& nk) {
+    while (s >= e) {
+      if (++r >= nruns) return false;
+      s = runs[2 * r];
+      e = runs[2 * r + 1];
+    }
+    start = s;
+    nk = min(BN, e - s);
+    s += BN;
+    return true;
+  }
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
+           const __grid_constant__ CUtensorMap tmv, const int32_t* __restrict__ qidx, int64_t L,
+           const ac_attn_item* __restrict__ items, const int32_t* __restrict__ runs,
+           float scale_log2, void* __restrict__ out, int out_dtype) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+  const ac_attn_item it = items[blockIdx.x];
+  if (it.q_rows <= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool two = it.q_rows > BM;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = bars + 1 + STAGES;
+  uint64_t* s_full = bars + 1 + 2 * STAGES;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_done = s_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_MISC);
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(kv_full + s, 1);
+      mbar_init(kv_empty + s, 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(s_full + t, 1);
+      mbar_init(p_full + t, 128);
+      mbar_init(o_done + t, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == W_MMA) tmem_alloc(tmem_slot, 512);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int32_t* iruns = runs + 2 * it.run0;
+  const int64_t krow0 = (int64_t)it.head * L;
+
+  if (warp == W_TMA) {
+    // ------------------------------ TMA producer ------------------------------
+    if (lane == 0) {
+      mbar_expect_tx(q_full, (two ? 2 : 1) * Q_BYTES);
+      tma_load_2d(sm + OFF_Q, &tmq, 0, (int)it.q_row0, q_full);
+      if (two) tma_load_2d(sm + OFF_Q + Q_BYTES, &tmq, 0, (int)it.q_row0 + BM, q_full);
+      TileIter ti(iruns, it.nruns);
+      int start, nk;
+      for (int j = 0; ti.next(start, nk); ++j) {
+        const int st = j % STAGES;
+        if (j >= STAGES) mbar_wait_sleep(kv_empty + st, ((j / STAGES) - 1) & 1, 40);
+        mbar_expect_tx(kv_full + st, 2 * KV_BYTES);
+        const int row = (int)(krow0 + start);
+        tma_load_2d(sm + OFF_K + st * KV_BYTES, &tmk, 0, row, kv_full + st);
+        tma_load_2d(sm + OFF_V + st * KV_BYTES, &tmv, 0, row, kv_full + st);
+      }
+    }
+    __syncwarp();
+  } else if (warp == W_MMA) {
+    // ------------------------------ MMA issuer --------------------------------
+    if (lane == 0) {
+      constexpr uint32_t IS = idesc_bf16(BM, BN, false);
+      constexpr uint32_t IO = idesc_bf16(BM, D, true);
+      const uint32_t sq = smem_u32(sm + OFF_Q);
+      auto issue_s = [&](int t, int st) {
+        const uint32_t sk = smem_u32(sm + OFF_K + st * KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t ad = sdesc(sq + t * Q_BYTES + kk * 32, 16, 1024);
+          const uint64_t bd = sdesc(sk + kk * 32, 16, 1024);
+          umma_f16(tmem + COL_S + t * BN, ad, bd, IS, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full + t);
+      };
+      auto issue_pv = [&](int t, int j, int st) {
+        mbar_wait_sleep(p_full + t, j & 1, 41);
+        fence_after();
+        const uint32_t sv = smem_u32(sm + OFF_V + st * KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t bd = sdesc(sv + kk * 2048, BN * 128, 1024);
+          umma_ts(tmem + COL_O + t * D, tmem + COL_P + t * 64 + kk * 8, bd, IO,
+                  (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(o_done + t);
+      };
+      mbar_wait_sleep(q_full, 0, 42);
+      TileIter ti(iruns, it.nruns);
+      int start, nk, j = 0;
+      while (ti.next(start, nk)) {
+        const int st = j % STAGES;
+        mbar_wait_sleep(kv_full + st, (j / STAGES) & 1, 43);
+        fence_after();
+        if (j > 0) issue_pv(0, j - 1, (j - 1) % STAGES);
+        issue_s(0, st);
+        if (two) {
+          if (j > 0) issue_pv(1, j - 1, (j - 1) % STAGES);
+          issue_s(1, st);
+        }
+        if (j > 0) umma_commit(kv_empty + (j - 1) % STAGES);
+        ++j;
+      }
+      if (j > 0) {
+        issue_pv(0, j - 1, (j - 1) % STAGES);
+        if (two) issue_pv(1, j - 1, (j - 1) % STAGES);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------ softmax ------------------------------
+    const int t = warp >> 2;  // Q tile of this warpgroup
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;  // TMEM lane / row in the tile
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tS = tmem + lane_base + COL_S + t * BN;
+    const uint32_t tO = tmem + lane_base + COL_O + t * D;
+    const uint32_t tP = tmem + lane_base + COL_P + t * 64;
+    float m_run = -INFINITY, l_run = 0.f;
+    int j = 0;
+    if (t == 0 || two) {
+      TileIter ti(iruns, it.nruns);
+      int start, nk;
+      while (ti.next(start, nk)) {
+        mbar_wait_sleep(s_full + t, j & 1, 44);
+        fence_after();
+        // pass 1: row max over the tile (S stays in TMEM; re-read in pass 2)
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t sr[32];
+          tmem_ld32(tS + c0, sr);
+          tmem_wait_ld();
+          if (nk < c0 + 32) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u)
+              if (c0 + u >= nk) sr[u] = __float_as_uint(-INFINITY);
+          }
+#pragma unroll
+          for (int u = 0; u < 32; u += 8) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+              mx[a] = fmaxf(mx[a], fmaxf(__uint_as_float(sr[u + 2 * a]), __uint_as_float(sr[u + 2 * a + 1])));
+          }
+        }
+        const float ms = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
+        // P_t / O_t are free once the previous tile's PV has completed
+        if (j > 0) {
+          mbar_wait_sleep(o_done + t, (j - 1) & 1, 45);
+          fence_after();
+        }
+        const bool need = ms > m_run + 8.f;
+        if (__any_sync(0xffffffffu, need)) {
+          float alpha = 1.f;
+          if (need) {
+            alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - ms);
+            l_run *= alpha;
+            m_run = ms;
+          }
+          if (j > 0) {
+#pragma unroll
+            for (int c0 = 0; c0 < D; c0 += 32) {
+              uint32_t r[32];
+              tmem_ld32(tO + c0, r);
+              tmem_wait_ld();
+#pragma unroll
+              for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * alpha);
+              tmem_st32(tO + c0, r);
+            }
+          }
+        }
+        const uint64_t sc = pk2(scale_log2, scale_log2);
+        const uint64_t nm = pk2(-m_run, -m_run);
+        uint64_t acc0 = pk2(0.f, 0.f), acc1 = pk2(0.f, 0.f);
+#pragma unroll
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          uint32_t sr[32];
+          tmem_ld32(tS + ch * 32, sr);
+          tmem_wait_ld();
+          if (nk < ch * 32 + 32) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u)
+              if (ch * 32 + u >= nk) sr[u] = __float_as_uint(-INFINITY);
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint64_t x = fma2(pk2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), sc, nm);
+            float x0, x1, p0, p1;
+            up2(x, x0, x1);
+            if ((i & 7) < 3) {
+              exp2_poly2(x0, x1, p0, p1);
+            } else {
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            if (i & 1) acc1 = add2(acc1, pk2(p0, p1));
+            else acc0 = add2(acc0, pk2(p0, p1));
+            pk[i] = pack_bf16(p0, p1);
+          }
+          tmem_st16(tP + ch * 16, pk);
+        }
+        float a0, a1, b0, b1;
+        up2(acc0, a0, a1);
+        up2(acc1, b0, b1);
+        l_run += (a0 + a1) + (b0 + b1);
+        tmem_wait_st();
+        fence_before();
+        mbar_arrive(p_full + t);
+        ++j;
+      }
+      // ------------------------------ epilogue ------------------------------
+      if (j > 0) {
+        mbar_wait_sleep(o_done + t, (j - 1) & 1, 46);
+        fence_after();
+      }
+      const int rows_t = min(BM, it.q_rows - t * BM);
+      const int tok = (row < rows_t) ? qidx[it.q_row0 + t * BM + row] : -1;
+      const float inv = (l_run > 0.f) ? 1.f / l_run : 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t r[32];
+        if (j > 0) {
+          tmem_ld32(tO + c0, r);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int u = 0; u < 32; ++u) r[u] = 0u;
+        }
+        if (tok >= 0) {
+          const int64_t ob = ((int64_t)it.head * L + tok) * D + c0;
+          if (out_dtype == AC_DTYPE_BF16) {
+            uint32_t w[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+              w[u] = pack_bf16(__uint_as_float(r[2 * u]) * inv, __uint_as_float(r[2 * u + 1]) * inv);
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + ob);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dst[u] = make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
+          } else {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + ob);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              dst[u] = make_float4(__uint_as_float(r[4 * u]) * inv, __uint_as_float(r[4 * u + 1]) * inv,
+                                   __uint_as_float(r[4 * u + 2]) * inv, __uint_as_float(r[4 * u + 3]) * inv);
+          }
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == W_MMA) {
+    fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace fa
+}  // namespace ac
+
+extern "C" int ac_sparse_attention_fa4(const void* q, int64_t q_rows_total, const int32_t* qidx,
+                                       const void* k, const void* v, int d, int64_t L, int heads,
+                                       const ac_attn_item* items, int nitems, const int32_t* runs,
+                                       float scale, void* out, int out_dtype, void* stream) {
+  using namespace ac::fa;
+  if (nitems <= 0) return AC_OK;
+  if (d != D) {
+    ac_host::set_error("fa4 attention: head_dim %d unsupported (64)", d);
+    return AC_ERR_DIM;
+  }
+  CUtensorMap mq, mk, mv;
+  int rc;
+  if ((rc = ac_host::make_map_2d(&mq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q_rows_total, D, 64, BM)))
+    return rc;
+  if ((rc = ac_host::make_map_2d(&mk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (int64_t)heads * L, D, 64, BN)))
+    return rc;
+  if ((rc = ac_host::make_map_2d(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (int64_t)heads * L, D, 64, BN)))
+    return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_attn_fa4,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return ac_host::check_cuda(e, "k_attn_fa4 smem");
+    attr = true;
+  }
+  const float scale_log2 = scale * 1.4426950408889634f;
+  k_attn_fa4<<<nitems, THREADS, SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(
+      mq, mk, mv, qidx, L, items, runs, scale_log2, out, out_dtype);
+  AC_CHECK_LAUNCH("k_attn_fa4");
+  return AC_OK;
+}

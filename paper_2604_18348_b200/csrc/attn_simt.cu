@@ -48,7 +48,7 @@ __global__ void k_q_layout_items(int64_t L, const int32_t* __restrict__ qcounts,
                                  const int32_t* __restrict__ gq, int gq_max,
                                  const int32_t* __restrict__ nruns, int topk_max,
                                  int64_t qp_cap, int32_t* __restrict__ padstart,
-                                 ac_attn_item* __restrict__ items, int item_cap) {
+                                 ac_attn_item* __restrict__ items, int item_cap, int item_rows) {
   const int h = blockIdx.x;
   const int G = gq[h];
   if (threadIdx.x != 0) return;
@@ -58,11 +58,11 @@ __global__ void k_q_layout_items(int64_t L, const int32_t* __restrict__ qcounts,
   for (int g = 0; g < G; ++g) {
     const int cnt = qcounts[(int64_t)h * gq_max + g];
     padstart[(int64_t)h * gq_max + g] = (int32_t)rowpos;
-    for (int r0 = 0; r0 < cnt; r0 += 128) {
+    for (int r0 = 0; r0 < cnt; r0 += item_rows) {
       if (it < item_cap) {
         ac_attn_item m;
         m.q_row0 = (int64_t)h * qp_cap + rowpos + r0;
-        m.q_rows = min(128, cnt - r0);
+        m.q_rows = min(item_rows, cnt - r0);
         m.head = h;
         m.run0 = (h * gq_max + g) * topk_max;
         m.nruns = nruns[(int64_t)h * gq_max + g];
@@ -94,14 +94,15 @@ __global__ void k_q_layout_rows(const void* __restrict__ q, int dtype, int d, in
   const int64_t row = (int64_t)h * qp_cap + padstart[(int64_t)h * gq_max + g] + local;
   qidx[row] = tok;
   const int64_t src = ((int64_t)h * L + tok) * d, dst = row * d;
-  if (dtype == AC_DTYPE_BF16) {
-    const __nv_bfloat16* s = reinterpret_cast<const __nv_bfloat16*>(q) + src;
-    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(qp) + dst;
-    for (int t = 0; t < d; ++t) o[t] = s[t];
+  const int esz = dtype == AC_DTYPE_BF16 ? 2 : 4;
+  const char* sp = reinterpret_cast<const char*>(q) + src * esz;
+  char* op = reinterpret_cast<char*>(qp) + dst * esz;
+  const int bytes = d * esz;
+  if ((bytes & 15) == 0 && ((reinterpret_cast<uintptr_t>(sp) | reinterpret_cast<uintptr_t>(op)) & 15) == 0) {
+    for (int o = 0; o < bytes; o += 16)
+      *reinterpret_cast<uint4*>(op + o) = *reinterpret_cast<const uint4*>(sp + o);
   } else {
-    const float* s = reinterpret_cast<const float*>(q) + src;
-    float* o = reinterpret_cast<float*>(qp) + dst;
-    for (int t = 0; t < d; ++t) o[t] = s[t];
+    for (int o = 0; o < bytes; ++o) op[o] = sp[o];
   }
 }
 
@@ -297,8 +298,12 @@ extern "C" int ac_build_q_layout(const void* q, int dtype, int d, int64_t L, int
                                  const int32_t* qcounts, const int32_t* qlabels, const int32_t* gq,
                                  int gq_max, const int32_t* nruns, int topk_max, void* qp,
                                  int32_t* qidx, int64_t qp_cap, ac_attn_item* items, int item_cap,
-                                 void* stream) {
+                                 int item_rows, void* stream) {
   if (heads <= 0 || L <= 0) return AC_OK;
+  if (item_rows != 128 && item_rows != 256) {
+    ac_host::set_error("ac_build_q_layout: item_rows must be 128 or 256");
+    return AC_ERR_PARAM;
+  }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int32_t* padstart = nullptr;
   // padstart lives right after qidx's used range: callers size qidx as
@@ -306,7 +311,7 @@ extern "C" int ac_build_q_layout(const void* q, int dtype, int d, int64_t L, int
   padstart = qidx + (int64_t)heads * qp_cap;
   cudaMemsetAsync(qidx, 0xff, sizeof(int32_t) * (size_t)heads * qp_cap, st);
   k_q_layout_items<<<heads, 32, 0, st>>>(L, qcounts, gq, gq_max, nruns, topk_max, qp_cap, padstart,
-                                         items, item_cap);
+                                         items, item_cap, item_rows);
   k_q_layout_rows<<<dim3((unsigned)((L + 255) / 256), heads), 256, 0, st>>>(
       q, dtype, d, L, qperm, qstarts, qlabels, gq_max, padstart, qp, qidx, qp_cap);
   AC_CHECK_LAUNCH("ac_build_q_layout");

@@ -178,12 +178,19 @@ extern "C" int ac_gemm_order(int64_t m, int64_t n, int64_t d) {
 // attention dispatch: tcgen05 kernel for bf16 / D in {64,128}, CUDA cores
 // otherwise (f32 inputs need f32 numerics for the 1e-4 parity bar)
 // ---------------------------------------------------------------------------
+extern "C" int ac_attention_item_rows(int dtype, int d) {
+  return (dtype == AC_DTYPE_BF16 && d == 64) ? 256 : 128;
+}
+
 extern "C" int ac_sparse_attention(const void* q, int64_t q_rows_total, const int32_t* qidx,
                                    const void* k, const void* v, int dtype, int d, int64_t L,
                                    int heads, const ac_attn_item* items, int nitems,
                                    const int32_t* runs, float scale, void* out, int out_dtype,
                                    void* stream) {
-  if (dtype == AC_DTYPE_BF16 && (d == 64 || d == 128))
+  if (dtype == AC_DTYPE_BF16 && d == 64)
+    return ac_sparse_attention_fa4(q, q_rows_total, qidx, k, v, d, L, heads, items, nitems, runs,
+                                   scale, out, out_dtype, stream);
+  if (dtype == AC_DTYPE_BF16 && d == 128)
     return ac_sparse_attention_tc(q, q_rows_total, qidx, k, v, d, L, heads, items, nitems, runs,
                                   scale, out, out_dtype, stream);
   return ac_sparse_attention_simt(q, qidx, k, v, dtype, d, L, items, nitems, runs, scale, out,

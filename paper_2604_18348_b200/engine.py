@@ -617,12 +617,14 @@ def sparse_attention_heads(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
         qstarts[h, :m.k + 1] = m.starts
     qp_cap = Ln + TILE * gq_max
     item_cap = (Ln + TILE - 1) // TILE + gq_max
+    item_rows = 128 if impl == "simt" else int(L.lib().ac_attention_item_rows(dt, da))
     qp = torch.empty((H * qp_cap, da), dtype=q.dtype, device=dev)
     qidx = torch.empty(H * qp_cap + H * gq_max, dtype=I32, device=dev)
     items = torch.empty(H * item_cap * L.ITEM_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     L.call("ac_build_q_layout", qa.data_ptr(), dt, da, Ln, H, qperm.data_ptr(), qstarts.data_ptr(),
            qcounts.data_ptr(), qlab.data_ptr(), gq.data_ptr(), gq_max, nruns.data_ptr(), topk_max,
-           qp.data_ptr(), qidx.data_ptr(), qp_cap, items.data_ptr(), item_cap, L.stream_ptr())
+           qp.data_ptr(), qidx.data_ptr(), qp_cap, items.data_ptr(), item_cap, item_rows,
+           L.stream_ptr())
     out = torch.empty((H, Ln, da), dtype=out_dtype, device=dev)
     odt = L.dtype_code(out) if out_dtype != F32 else L.DTYPE_F32
     scale = float(1.0 / math.sqrt(D))
