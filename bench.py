@@ -325,41 +325,38 @@ def main():
         gather(sess.step(*dev_in[(i + 1) % 2]))
     barrier()
 
-    # ---- timed warm steps (device-resident inputs) ----
-    lasts = []
-    timer = PhaseTimer()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    with ClockSampler(local) as clocks, timer:
+    # ---- timed warm steps (device-resident inputs; one CUDA graph per step) ----
+    with ClockSampler(local) as clocks:
         barrier()
         start = torch.cuda.Event(enable_timing=True)
         stop = torch.cuda.Event(enable_timing=True)
         start.record()
         for i in range(args.steps):
-            ev[i][0].record()
             out = gather(sess.step(*dev_in[(args.warmup + i + 1) % 2]))
-            ev[i][1].record()
-            lasts.append(sess.last)
         stop.record()
         barrier()
     total_ms = start.elapsed_time(stop)
     ms_local = total_ms / max(args.steps, 1)
     ms = ms_local
-    phases = timer.summary()
     if world > 1:
         tt = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    attn_ms = phases.get("attention", 0.0) / max(args.steps, 1)
-    useful = (sum(float(attention_flops(l, D).item()) for l in lasts) / len(lasts)) if lasts else 0.0
-    del lasts
-
+    # attention kernel time: CUDA events recorded inside the graph around the
+    # kernel, on its stream (last timed step); useful FLOPs of that step
+    if sess.steady is not None:
+        attn_ms = sess.steady.last_times_ms()["attention"]
+    else:
+        attn_ms = 0.0
+    useful = sess.useful_attention_flops()
     # ---- launches per step (profiler replica of one step, untimed) ----
     launches = count_launches(sess, dev_in, gather, args) * args.steps
 
     # ---- e2e through the public API with pinned host buffers ----
     e2e = None
     if not args.no_e2e:
+        for i in range(args.warmup):
+            sess.step(*host[(i + 1) % 2])
         barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
@@ -381,6 +378,18 @@ def main():
                "d2h_bytes_per_step": len(my) * Ln * D * esz,
                "api": "paper_2604_18348_b200.LayerSession.step(host pinned Q/K/V)"}
 
+    phases = {}
+    if args.breakdown:  # eager replica of one warm step with per-phase events
+        timer = PhaseTimer()
+        sess.graph = False
+        steady, sess.steady = sess.steady, None
+        if steady is not None:
+            sess.key_centers, sess.query_centers = steady.key_centers(), steady.query_centers()
+        with timer:
+            sess.step(*dev_in[0])
+        phases = timer.summary()
+        sess.graph = True
+        sess.steady = None
     # ---- dense baseline (torch SDPA: cuDNN / flash on sm_100) ----
     dense = None
     if not args.no_dense and rank == 0 and my:
@@ -415,9 +424,9 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "cold_step_ms": cold_ms,
-            "phases_ms_per_step": {k: v / max(args.steps, 1) for k, v in phases.items()},
+            "phases_ms_eager_step": phases,
             "dense_sdpa_ms": dense,
-            "density": float(sess.last[2].selections[0].density.item()) if sess.last else None,
+            "density": sess.density(),
         }
         if args.breakdown:
             line["cold_phases_ms"] = cold_breakdown

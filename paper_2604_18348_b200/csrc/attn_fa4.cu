@@ -44,7 +44,7 @@ constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
 constexpr int OFF_V = OFF_K + STAGES * KV_BYTES;
 constexpr int OFF_BAR = OFF_V + STAGES * KV_BYTES;
-constexpr int NBAR = 1 + 2 * STAGES + 2 + 2 + 2;
+constexpr int NBAR = 1 + 2 * STAGES + 2 + 2 + 2 + 2;
 constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
 constexpr int SMEM = OFF_MISC + 16 + 1024;
 constexpr uint32_t COL_S = 0, COL_O = 256, COL_P = 384;
@@ -57,7 +57,8 @@ AC_DEV void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t i
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
 }
-AC_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+// the first 16 words of r
+AC_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
       "%14,%15,%16};\n" ::"r"(taddr),
@@ -157,6 +158,7 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
   uint64_t* s_full = bars + 1 + 2 * STAGES;
   uint64_t* p_full = s_full + 2;
   uint64_t* o_done = s_full + 4;
+  uint64_t* s_free = s_full + 6;  // softmax has S_t in registers: the MMA may overwrite it
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_MISC);
 
   if (threadIdx.x == 0) {
@@ -169,6 +171,7 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
       mbar_init(s_full + t, 1);
       mbar_init(p_full + t, 128);
       mbar_init(o_done + t, 1);
+      mbar_init(s_free + t, 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -204,7 +207,8 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
       constexpr uint32_t IS = idesc_bf16(BM, BN, false);
       constexpr uint32_t IO = idesc_bf16(BM, D, true);
       const uint32_t sq = smem_u32(sm + OFF_Q);
-      auto issue_s = [&](int t, int st) {
+      auto issue_s = [&](int t, int j, int st) {
+        if (j > 0) mbar_wait_sleep(s_free + t, (j - 1) & 1, 47);
         const uint32_t sk = smem_u32(sm + OFF_K + st * KV_BYTES);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -233,11 +237,13 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
         const int st = j % STAGES;
         mbar_wait_sleep(kv_full + st, (j / STAGES) & 1, 43);
         fence_after();
-        if (j > 0) issue_pv(0, j - 1, (j - 1) % STAGES);
-        issue_s(0, st);
-        if (two) {
-          if (j > 0) issue_pv(1, j - 1, (j - 1) % STAGES);
-          issue_s(1, st);
+        // S for tile j as soon as each softmax has pulled S_{j-1} into
+        // registers, then the PV products of tile j-1 once P_{j-1} is in TMEM
+        issue_s(0, j, st);
+        if (two) issue_s(1, j, st);
+        if (j > 0) {
+          issue_pv(0, j - 1, (j - 1) % STAGES);
+          if (two) issue_pv(1, j - 1, (j - 1) % STAGES);
         }
         if (j > 0) umma_commit(kv_empty + (j - 1) % STAGES);
         ++j;
@@ -265,68 +271,52 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
       while (ti.next(start, nk)) {
         mbar_wait_sleep(s_full + t, j & 1, 44);
         fence_after();
-        // pass 1: row max over the tile (S stays in TMEM; re-read in pass 2)
-        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        uint32_t sr[BN / 32][32];
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          uint32_t sr[32];
-          tmem_ld32(tS + c0, sr);
-          tmem_wait_ld();
-          if (nk < c0 + 32) {
+        for (int ch = 0; ch < BN / 32; ++ch) tmem_ld32(tS + ch * 32, sr[ch]);
+        tmem_wait_ld();
+        fence_before();
+        mbar_arrive(s_free + t);
+        if (nk < BN) {
+#pragma unroll
+          for (int ch = 0; ch < BN / 32; ++ch)
 #pragma unroll
             for (int u = 0; u < 32; ++u)
-              if (c0 + u >= nk) sr[u] = __float_as_uint(-INFINITY);
-          }
+              if (ch * 32 + u >= nk) sr[ch][u] = __float_as_uint(-INFINITY);
+        }
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int u = 0; u < 32; u += 8) {
+        for (int ch = 0; ch < BN / 32; ++ch)
+#pragma unroll
+          for (int u = 0; u < 32; u += 8)
 #pragma unroll
             for (int a = 0; a < 4; ++a)
-              mx[a] = fmaxf(mx[a], fmaxf(__uint_as_float(sr[u + 2 * a]), __uint_as_float(sr[u + 2 * a + 1])));
-          }
-        }
+              mx[a] = fmaxf(mx[a], fmaxf(__uint_as_float(sr[ch][u + 2 * a]),
+                                         __uint_as_float(sr[ch][u + 2 * a + 1])));
         const float ms = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
         // P_t / O_t are free once the previous tile's PV has completed
         if (j > 0) {
           mbar_wait_sleep(o_done + t, (j - 1) & 1, 45);
           fence_after();
         }
+        // lazy rescale: a row's running max only moves when it grows by > 2^8
         const bool need = ms > m_run + 8.f;
-        if (__any_sync(0xffffffffu, need)) {
-          float alpha = 1.f;
-          if (need) {
-            alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - ms);
-            l_run *= alpha;
-            m_run = ms;
-          }
-          if (j > 0) {
-#pragma unroll
-            for (int c0 = 0; c0 < D; c0 += 32) {
-              uint32_t r[32];
-              tmem_ld32(tO + c0, r);
-              tmem_wait_ld();
-#pragma unroll
-              for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * alpha);
-              tmem_st32(tO + c0, r);
-            }
-          }
+        const bool warp_need = __any_sync(0xffffffffu, need);
+        float alpha = 1.f;
+        if (need) {
+          alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - ms);
+          l_run *= alpha;
+          m_run = ms;
         }
         const uint64_t sc = pk2(scale_log2, scale_log2);
         const uint64_t nm = pk2(-m_run, -m_run);
         uint64_t acc0 = pk2(0.f, 0.f), acc1 = pk2(0.f, 0.f);
 #pragma unroll
         for (int ch = 0; ch < BN / 32; ++ch) {
-          uint32_t sr[32];
-          tmem_ld32(tS + ch * 32, sr);
-          tmem_wait_ld();
-          if (nk < ch * 32 + 32) {
-#pragma unroll
-            for (int u = 0; u < 32; ++u)
-              if (ch * 32 + u >= nk) sr[u] = __float_as_uint(-INFINITY);
-          }
-          uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const uint64_t x = fma2(pk2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), sc, nm);
+            const uint64_t x =
+                fma2(pk2(__uint_as_float(sr[ch][2 * i]), __uint_as_float(sr[ch][2 * i + 1])), sc, nm);
             float x0, x1, p0, p1;
             up2(x, x0, x1);
             if ((i & 7) < 3) {
@@ -337,15 +327,27 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
             }
             if (i & 1) acc1 = add2(acc1, pk2(p0, p1));
             else acc0 = add2(acc0, pk2(p0, p1));
-            pk[i] = pack_bf16(p0, p1);
+            sr[ch][i] = pack_bf16(p0, p1);  // packed P overwrites consumed S slots
           }
-          tmem_st16(tP + ch * 16, pk);
+          tmem_st16(tP + ch * 16, sr[ch]);
         }
         float a0, a1, b0, b1;
         up2(acc0, a0, a1);
         up2(acc1, b0, b1);
         l_run += (a0 + a1) + (b0 + b1);
         tmem_wait_st();
+        if (warp_need && j > 0) {  // O_t *= alpha before PV_j accumulates into it
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tO + c0, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * alpha);
+            tmem_st32(tO + c0, r);
+          }
+          tmem_wait_st();
+        }
         fence_before();
         mbar_arrive(p_full + t);
         ++j;

@@ -402,7 +402,7 @@ class LayerSession:
 
     def __init__(self, params: PipelineParams | None = None, seed: int = 0, layer: int = 0,
                  out_dtype=None, attn_impl: str = "auto", head_offset: int = 0,
-                 reduce_flag=None):
+                 reduce_flag=None, graph: bool = True):
         self.reduce_flag = reduce_flag or (lambda local: local)
         self.params = params or PipelineParams()
         self.params.validate()
@@ -411,15 +411,60 @@ class LayerSession:
         self.attn_impl = attn_impl
         self.t = 0
         self.mode = None
-        self.key_centers = None
-        self.query_centers = None
+        self._key_centers = None
+        self._query_centers = None
         self.last = None
+        self.graph = graph
+        self.steady = None  # SteadyStep (CUDA graph) once the warm step is fixed
+
+    # carried state (pipeline.py:85-90); lives in the steady step's batches
+    @property
+    def key_centers(self):
+        return self.steady.key_centers() if self.steady is not None else self._key_centers
+
+    @key_centers.setter
+    def key_centers(self, v):
+        self._key_centers = v
+
+    @property
+    def query_centers(self):
+        return self.steady.query_centers() if self.steady is not None else self._query_centers
+
+    @query_centers.setter
+    def query_centers(self, v):
+        self._query_centers = v
+
+    def useful_attention_flops(self) -> float:
+        """4·D·Σ_heads Σ_g |Q_g|·|S_g| of the last sparse step (no tile padding)."""
+        if self.steady is not None:
+            return float(self.steady.useful_attention_flops().item())
+        if self.last is None:
+            return 0.0
+        qm, _, so = self.last
+        D = so.out.shape[-1]
+        tot = sum(float((m.counts.double() * sel._covered.double()).sum().item())
+                  for m, sel in zip(qm, so.selections))
+        return tot * 4.0 * D
+
+    def density(self) -> float:
+        if self.steady is not None:
+            return float(self.steady.density[0].item())
+        if self.last is None:
+            return float("nan")
+        return float(self.last[2].selections[0].density.item())
 
     def step(self, Q, K, V):
         host = not (isinstance(Q, torch.Tensor) and Q.device.type == "cuda")
         dev = L.device()
         if host:
-            Q, K, V = (torch.as_tensor(x).to(dev, non_blocking=True) for x in (Q, K, V))
+            st = self.steady
+            Q, K, V = (torch.as_tensor(x) for x in (Q, K, V))
+            if st is not None and st.Q.shape == Q.shape and st.dtype == Q.dtype:
+                for dst, src in ((st.Q, Q), (st.K, K), (st.V, V)):  # straight into the graph inputs
+                    dst.copy_(src, non_blocking=True)
+                Q, K, V = st.Q, st.K, st.V
+            else:
+                Q, K, V = (x.to(dev, non_blocking=True) for x in (Q, K, V))
         odt = self.out_dtype or (torch.bfloat16 if Q.dtype == torch.bfloat16 else torch.float32)
         run = LayerRunner(self.params, odt, self.attn_impl)
         H = Q.shape[0]
@@ -442,6 +487,18 @@ class LayerSession:
         elif self.mode == "full":
             with phase("attention_dense"):
                 out = run.dense(Q, K, V)
+        elif self.graph and self.attn_impl == "auto" and self.params.scorer == "quest":
+            from .steady import SteadyStep
+            if self.steady is None or self.steady.Q.shape != Q.shape or self.steady.dtype != Q.dtype:
+                kc, qc = self.key_centers, self.query_centers
+                self.steady = None
+                self.steady = SteadyStep(H, Q.shape[1], Q.shape[2], Q.dtype, self.params, kc, qc,
+                                         odt)
+                self.last = None
+            with phase("steady_step"):
+                out = self.steady.step(Q, K, V)
+            if not host:
+                out = out.clone()  # the graph's output buffer is reused next step
         else:
             qm, reps, km = run.warm(Q, K, self.key_centers, self.query_centers)
             so = run.sparse(Q, K, V, qm, reps, km, self.params.topk)

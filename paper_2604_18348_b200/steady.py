@@ -1,0 +1,223 @@
+"""Steady-state denoising step of one layer as a single CUDA graph.
+
+After step 0 the reference's per-head work is fixed in shape
+(pipeline.py:344-385, t >= 1): warm-started key Lloyd from the carried
+centres (``warm_start_update``, clustering.py:170-179), warm-started query
+clustering (``cluster_queries(init_centers=...)``, clustering.py:182-200),
+envelopes + TensorQuest + top-k (quest.py:61-143) and the gathered sparse
+attention (pipeline.py:154-165).  Every data-dependent decision inside that
+step (Lloyd convergence, empty-cluster repair, run lengths, work items) is
+taken on the device, so the whole step is enqueued once, captured into a
+CUDA graph and replayed: no host synchronisation and no per-launch host work
+(descriptor uploads, TMA tensor-map encoding) in steady state.
+
+The clustering batches persist across steps: a Lloyd run leaves its final
+centres in the batch, which is exactly the next step's warm start
+(``_carry_centers`` is a passthrough for t >= 1, pipeline.py:223-234).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import engine as E
+
+F32 = torch.float32
+I32 = torch.int32
+
+
+class SteadyStep:
+    """Graph-captured warm step for H heads of [L, D] (bf16 or f32).
+
+    ``step(Q, K, V)`` copies the inputs into the graph's static buffers,
+    replays the graph and returns the static output buffer [H, L, D]
+    (valid until the next call)."""
+
+    def __init__(self, H: int, Ln: int, D: int, dtype: torch.dtype, params, key_centers: list,
+                 query_centers: list, out_dtype=None, use_graph: bool = True):
+        dev = L.device()
+        self.H, self.L, self.D, self.dtype = H, Ln, D, dtype
+        self.p = params
+        self.out_dtype = out_dtype or (torch.bfloat16 if dtype == torch.bfloat16 else F32)
+        self.Q = torch.empty((H, Ln, D), dtype=dtype, device=dev)
+        self.K = torch.empty((H, Ln, D), dtype=dtype, device=dev)
+        self.V = torch.empty((H, Ln, D), dtype=dtype, device=dev)
+        p = params
+        # ---- key clustering (warm Lloyd, in place across steps) ----
+        self.kb = E.Batch([self.K[h] for h in range(H)], [int(c.shape[0]) for c in key_centers],
+                          p.max_iter)
+        for h, c in enumerate(key_centers):
+            self.kb.centers_of(h).copy_(c.to(F32))
+        # ---- query clustering on the normalised queries ----
+        self.qn = torch.empty((H, Ln, D), dtype=F32, device=dev)
+        self.qdeg = torch.empty(H * Ln, dtype=torch.uint8, device=dev)
+        gq = {int(c.shape[0]) for c in query_centers}
+        if len(gq) != 1:
+            raise ValueError("steady step expects one query-cluster count for all heads")
+        self.gq = gq.pop()
+        self.qb = E.Batch([self.qn[h] for h in range(H)], [self.gq] * H, p.max_iter)
+        for h, c in enumerate(query_centers):
+            self.qb.centers_of(h).copy_(c.to(F32))
+        self.qmodels = [self.qb.model(h) for h in range(H)]
+        self.kmodels = [self.kb.model(h) for h in range(H)]
+        # ---- representatives (f64 member means) ----
+        self.reps = [torch.empty((self.gq, D), dtype=F32, device=dev) for _ in range(H)]
+        desc = np.zeros(H, dtype=L.PROBLEM_DTYPE)
+        for h, m in enumerate(self.qmodels):
+            e = desc[h]
+            e["x"] = self.qn[h].data_ptr()
+            e["counts"], e["perm"], e["starts"] = m.counts.data_ptr(), m.perm.data_ptr(), m.starts.data_ptr()
+            e["n"], e["k"] = m.n, m.k
+        self.reps_desc = L.to_device_struct(desc)
+        self.reps_ptrs = torch.tensor([r.data_ptr() for r in self.reps], dtype=torch.int64).to(dev)
+        # ---- envelopes ----
+        self.emax = [torch.empty((m.k, D), dtype=F32, device=dev) for m in self.kmodels]
+        self.emin = [torch.empty((m.k, D), dtype=F32, device=dev) for m in self.kmodels]
+        desc = np.zeros(H, dtype=L.PROBLEM_DTYPE)
+        for h, m in enumerate(self.kmodels):
+            e = desc[h]
+            e["x"] = self.K[h].data_ptr()
+            e["counts"], e["perm"], e["starts"] = m.counts.data_ptr(), m.perm.data_ptr(), m.starts.data_ptr()
+            e["n"], e["k"] = m.n, m.k
+        self.env_desc = L.to_device_struct(desc)
+        self.pmax = torch.tensor([t.data_ptr() for t in self.emax], dtype=torch.int64).to(dev)
+        self.pmin = torch.tensor([t.data_ptr() for t in self.emin], dtype=torch.int64).to(dev)
+        # ---- selection ----
+        self.topks = [min(p.topk, m.k) for m in self.kmodels]
+        self.stride = max(self.topks)
+        self.runs = torch.zeros((H, self.gq, self.stride, 2), dtype=I32, device=dev)
+        self.nruns = torch.zeros((H, self.gq), dtype=I32, device=dev)
+        self.scores = [torch.empty((self.gq, m.k), dtype=F32, device=dev) for m in self.kmodels]
+        self.selected = [torch.empty((self.gq, t), dtype=torch.int64, device=dev) for t in self.topks]
+        self.covered = torch.empty((H, self.gq), dtype=torch.int64, device=dev)
+        self.density = torch.empty((H,), dtype=torch.float64, device=dev)
+        desc = np.zeros(H, dtype=L.SELECT_DTYPE)
+        for h in range(H):
+            e = desc[h]
+            e["reps"] = self.reps[h].data_ptr()
+            e["emax"], e["emin"] = self.emax[h].data_ptr(), self.emin[h].data_ptr()
+            e["counts"], e["kstarts"] = self.kmodels[h].counts.data_ptr(), self.kmodels[h].starts.data_ptr()
+            e["scores"], e["selected"] = self.scores[h].data_ptr(), self.selected[h].data_ptr()
+            e["runs"], e["nruns"] = self.runs[h].data_ptr(), self.nruns[h].data_ptr()
+            e["covered"] = self.covered[h].data_ptr()
+            e["density"] = self.density[h:h + 1].data_ptr()
+            e["gq"], e["c"], e["topk"] = self.gq, self.kmodels[h].k, self.topks[h]
+            e["order"] = L.gemm_order(self.gq, self.kmodels[h].k, D)
+            e["run_stride"] = self.stride
+        self.sel_desc = L.to_device_struct(desc)
+        self.scorer = L.SCORERS[p.scorer]
+        if p.scorer != "quest":
+            raise ValueError("the graph-captured step implements the default 'quest' scorer")
+        # ---- attention buffers ----
+        da = E._attn_dim(D)
+        if da != D:
+            raise ValueError("graph-captured step needs head_dim in (16, 32, 64, 128)")
+        self.dt = L.dtype_code(self.Q)
+        self.kp = torch.empty_like(self.K)
+        self.vp = torch.empty_like(self.V)
+        self.kperm = self.kb.perm.view(H, Ln)
+        self.qperm = self.qb.perm.view(H, Ln)
+        self.qlab = self.qb.labels.view(H, Ln)
+        self.qcounts = self.qb.counts.view(H, self.gq)
+        self.qstarts = self.qb.starts.view(H, self.gq + 1)
+        self.gq_t = torch.full((H,), self.gq, dtype=I32, device=dev)
+        self.qp_cap = Ln + E.TILE * self.gq
+        self.item_cap = (Ln + E.TILE - 1) // E.TILE + self.gq
+        self.item_rows = int(L.lib().ac_attention_item_rows(self.dt, D))
+        self.qp = torch.empty((H * self.qp_cap, D), dtype=dtype, device=dev)
+        self.qidx = torch.empty(H * self.qp_cap + H * self.gq, dtype=I32, device=dev)
+        self.items = torch.empty(H * self.item_cap * L.ITEM_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        self.out = torch.empty((H, Ln, D), dtype=self.out_dtype, device=dev)
+        self.odt = L.dtype_code(self.out) if self.out_dtype != F32 else L.DTYPE_F32
+        self.scale = float(1.0 / math.sqrt(D))
+        self.graph = None
+        self.use_graph = use_graph
+        # CUDA events recorded inside the graph around the attention kernel
+        # and around the clustering (kernel time of the last replay)
+        self.ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
+
+    # ------------------------------------------------------------------
+    def _enqueue(self):
+        """Every kernel of one warm step, in order, on the current stream."""
+        H, Ln, D = self.H, self.L, self.D
+        p = self.p
+        s = L.stream_ptr()
+        kb, qb = self.kb, self.qb
+        self.ev[0].record()
+        L.call("ac_lloyd", *kb.args(), int(p.max_iter), float(p.tol), 0, kb.desc.ctypes.data, s)
+        L.call("ac_l2norm", self.Q.data_ptr(), self.dt, H * Ln, D, self.qn.data_ptr(), 0,
+               self.qdeg.data_ptr(), s)
+        L.call("ac_lloyd", *qb.args(), int(p.max_iter), float(p.tol), 0, qb.desc.ctypes.data, s)
+        L.call("ac_segment_mean", self.reps_desc.data_ptr(), H, L.DTYPE_F32, D, self.gq,
+               self.reps_ptrs.data_ptr(), s)
+        L.call("ac_envelopes", self.env_desc.data_ptr(), H, self.dt, D, kb.max_k,
+               self.pmax.data_ptr(), self.pmin.data_ptr(), s)
+        L.call("ac_select", self.sel_desc.data_ptr(), H, D, self.scorer, self.gq, kb.max_k,
+               self.stride, s)
+        L.call("ac_permute_rows_heads", self.K.data_ptr(), self.dt, D, self.kperm.data_ptr(), Ln, H,
+               self.kp.data_ptr(), s)
+        L.call("ac_permute_rows_heads", self.V.data_ptr(), self.dt, D, self.kperm.data_ptr(), Ln, H,
+               self.vp.data_ptr(), s)
+        L.call("ac_build_q_layout", self.Q.data_ptr(), self.dt, D, Ln, H, self.qperm.data_ptr(),
+               self.qstarts.data_ptr(), self.qcounts.data_ptr(), self.qlab.data_ptr(),
+               self.gq_t.data_ptr(), self.gq, self.nruns.data_ptr(), self.stride,
+               self.qp.data_ptr(), self.qidx.data_ptr(), self.qp_cap, self.items.data_ptr(),
+               self.item_cap, self.item_rows, s)
+        self.ev[1].record()
+        L.call("ac_sparse_attention", self.qp.data_ptr(), H * self.qp_cap, self.qidx.data_ptr(),
+               self.kp.data_ptr(), self.vp.data_ptr(), self.dt, D, Ln, H, self.items.data_ptr(),
+               H * self.item_cap, self.runs.data_ptr(), self.scale, self.out.data_ptr(), self.odt, s)
+        self.ev[2].record()
+
+    def _capture(self):
+        # one eager run on a side stream (lazy kernel attributes, workspaces),
+        # then capture; the eager run advanced the warm start, so restore it
+        kc = self.kb.centers.clone()
+        qc = self.qb.centers.clone()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._enqueue()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.kb.centers.copy_(kc)
+        self.qb.centers.copy_(qc)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._enqueue()
+        torch.cuda.synchronize()
+        self.graph = g
+
+    def step(self, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor) -> torch.Tensor:
+        """One warm step; returns the static output buffer [H, L, D]."""
+        for dst, src in ((self.Q, Q), (self.K, K), (self.V, V)):
+            if src.data_ptr() != dst.data_ptr():
+                dst.copy_(src, non_blocking=True)
+        if not self.use_graph:
+            self._enqueue()
+        else:
+            if self.graph is None:
+                self._capture()
+            self.graph.replay()
+        return self.out
+
+    def last_times_ms(self) -> dict:
+        """Device time of the last step's phases (synchronises)."""
+        self.ev[2].synchronize()
+        return {"cluster_select_layout": self.ev[0].elapsed_time(self.ev[1]),
+                "attention": self.ev[1].elapsed_time(self.ev[2])}
+
+    # ---- state views (device tensors, valid after step) ----
+    def key_centers(self) -> list:
+        return [self.kb.centers_of(h).clone() for h in range(self.H)]
+
+    def query_centers(self) -> list:
+        return [self.qb.centers_of(h).clone() for h in range(self.H)]
+
+    def useful_attention_flops(self) -> torch.Tensor:
+        """4·D·Σ_h Σ_g |Q_g|·|S_g| of the last step (device scalar, f64)."""
+        return (self.qcounts.double() * self.covered.double()).sum() * 4.0 * self.D

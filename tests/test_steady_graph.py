@@ -1,0 +1,40 @@
+"""The graph-captured steady-state step (steady.py) equals the eager warm
+step bit for bit, step after step (same kernels, state carried in place)."""
+
+import dataclasses
+
+import pytest
+import torch
+
+from paper_2604_18348_b200.synthetic import CRIT7_SPEC, gen_synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_graph_step_matches_eager(gpu, dtype):
+    import paper_2604_18348_b200 as P
+    H, Ln, D, T = 3, 4096, 64, 4
+    spec = dataclasses.replace(CRIT7_SPEC, drift_sigma=5e-4)
+    steps = [[], [], [], []]
+    for h in range(H):
+        s = gen_synthetic(spec, Ln, D, 1, T, 100 + h)
+        for t in range(T):
+            steps[t].append(s[t][0])
+    ins = [[torch.stack([torch.from_numpy(x[j]) for x in steps[t]]).to(dtype).cuda()
+            for j in range(3)] for t in range(T)]
+    params = P.PipelineParams(q_clusters=65, topk=25, full_layer_quota=0.0)
+    eager = P.LayerSession(params, graph=False)
+    graph = P.LayerSession(params, graph=True)
+    for t in range(T):
+        a = eager.step(*ins[t])
+        b = graph.step(*ins[t])
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), f"step {t}: outputs differ"
+        for x, y in zip(eager.key_centers, graph.key_centers):
+            assert torch.equal(x, y), f"step {t}: key centres differ"
+        for x, y in zip(eager.query_centers, graph.query_centers):
+            assert torch.equal(x, y), f"step {t}: query centres differ"
+    assert graph.steady is not None and graph.steady.graph is not None
+    assert graph.density() == pytest.approx(eager.density())
+    assert graph.useful_attention_flops() == pytest.approx(eager.useful_attention_flops())
