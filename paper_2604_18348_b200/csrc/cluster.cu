@@ -56,43 +56,59 @@ AC_DEV float ordered_dot(const GetX& gx, const GetC& gc, int d, int order, bool 
 // ---------------------------------------------------------------------------
 // K1: row squared norms and l2 normalisation (tensorops.py:59-76)
 // ---------------------------------------------------------------------------
-__global__ void k_row_sqnorm(const void* __restrict__ x, int dtype, int64_t rows,
-                             int d, float* __restrict__ out) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  const int64_t base = r * d;
-  auto get = [&](int i) {
-    float v = ld_elem(x, dtype, base + i);
-    return __fmul_rn(v, v);
-  };
-  out[r] = pw_sum<float>(get, d);
+// Rows are staged through shared memory (coalesced global access, padded
+// row stride d+1 so the thread-per-row pairwise sums are bank-conflict
+// free); every row's arithmetic is the reference's numpy order.
+constexpr int kNormRows = 128;
+
+AC_DEV void stage_rows_f32(const void* __restrict__ x, int dtype, int64_t row0, int rows, int d,
+                           float* s) {
+  const int ld = d + 1;
+  const int64_t base = row0 * d;
+  for (int e = threadIdx.x; e < rows * d; e += blockDim.x) {
+    const int r = e / d, t = e - r * d;
+    s[r * ld + t] = ld_elem(x, dtype, base + e);
+  }
 }
 
-__global__ void k_l2norm(const void* __restrict__ x, int dtype, int64_t rows, int d,
-                         float* __restrict__ out, float* __restrict__ out_sq,
-                         uint8_t* __restrict__ degenerate) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  const int64_t base = r * d;
-  auto get = [&](int i) {
-    float v = ld_elem(x, dtype, base + i);
-    return __fmul_rn(v, v);
-  };
-  const float norm = __fsqrt_rn(pw_sum<float>(get, d));
-  const bool degen = norm < 1e-12f;                       // DEGENERATE_NORM
-  const bool unit = fabsf(__fsub_rn(norm, 1.0f)) <= 2e-6f;  // already unit
-  const float safe = (degen || unit) ? 1.0f : norm;
-  for (int i = 0; i < d; ++i) {
-    float v = degen ? 0.f : __fdiv_rn(ld_elem(x, dtype, base + i), safe);
-    out[base + i] = v;
+AC_DEV float row_sq_pw(const float* s, int d) {
+  return pw_sum<float>([&](int i) { return __fmul_rn(s[i], s[i]); }, d);
+}
+
+__global__ void __launch_bounds__(kNormRows)
+k_row_sqnorm(const void* __restrict__ x, int dtype, int64_t rows, int d, float* __restrict__ out) {
+  extern __shared__ float nsm[];
+  const int64_t row0 = (int64_t)blockIdx.x * kNormRows;
+  const int nr = (int)min((int64_t)kNormRows, rows - row0);
+  stage_rows_f32(x, dtype, row0, nr, d, nsm);
+  __syncthreads();
+  if ((int)threadIdx.x < nr) out[row0 + threadIdx.x] = row_sq_pw(nsm + threadIdx.x * (d + 1), d);
+}
+
+__global__ void __launch_bounds__(kNormRows)
+k_l2norm(const void* __restrict__ x, int dtype, int64_t rows, int d, float* __restrict__ out,
+         float* __restrict__ out_sq, uint8_t* __restrict__ degenerate) {
+  extern __shared__ float nsm[];
+  const int ld = d + 1;
+  const int64_t row0 = (int64_t)blockIdx.x * kNormRows;
+  const int nr = (int)min((int64_t)kNormRows, rows - row0);
+  stage_rows_f32(x, dtype, row0, nr, d, nsm);
+  __syncthreads();
+  const int r = threadIdx.x;
+  if (r < nr) {
+    float* s = nsm + r * ld;
+    const float norm = __fsqrt_rn(row_sq_pw(s, d));
+    const bool degen = norm < 1e-12f;                         // DEGENERATE_NORM
+    const bool unit = fabsf(__fsub_rn(norm, 1.0f)) <= 2e-6f;  // already unit
+    const float safe = (degen || unit) ? 1.0f : norm;
+    for (int i = 0; i < d; ++i) s[i] = degen ? 0.f : __fdiv_rn(s[i], safe);
+    if (degenerate) degenerate[row0 + r] = degen ? 1 : 0;
+    if (out_sq) out_sq[row0 + r] = row_sq_pw(s, d);
   }
-  if (degenerate) degenerate[r] = degen ? 1 : 0;
-  if (out_sq) {
-    auto geto = [&](int i) {
-      float v = out[base + i];
-      return __fmul_rn(v, v);
-    };
-    out_sq[r] = pw_sum<float>(geto, d);
+  __syncthreads();
+  for (int e = threadIdx.x; e < nr * d; e += blockDim.x) {
+    const int rr = e / d, t = e - rr * d;
+    out[row0 * d + e] = nsm[rr * ld + t];
   }
 }
 
@@ -107,17 +123,16 @@ __global__ void k_center_sqnorm(const ac_cluster_problem* __restrict__ probs, in
   P.cc[c] = pw_sum<float>(get, d);
 }
 
-__global__ void k_problem_xx(const ac_cluster_problem* __restrict__ probs, int dtype,
-                             int d) {
+__global__ void __launch_bounds__(kNormRows)
+k_problem_xx(const ac_cluster_problem* __restrict__ probs, int dtype, int d) {
+  extern __shared__ float nsm[];
   const ac_cluster_problem& P = probs[blockIdx.y];
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= P.n) return;
-  const int64_t base = r * d;
-  auto get = [&](int i) {
-    float v = ld_elem(P.x, dtype, base + i);
-    return __fmul_rn(v, v);
-  };
-  P.xx[r] = pw_sum<float>(get, d);
+  const int64_t row0 = (int64_t)blockIdx.x * kNormRows;
+  if (row0 >= P.n) return;
+  const int nr = (int)min((int64_t)kNormRows, P.n - row0);
+  stage_rows_f32(P.x, dtype, row0, nr, d, nsm);
+  __syncthreads();
+  if ((int)threadIdx.x < nr) P.xx[row0 + threadIdx.x] = row_sq_pw(nsm + threadIdx.x * (d + 1), d);
 }
 
 __global__ void k_status_init(const ac_cluster_problem* __restrict__ probs, int nprob) {
@@ -503,20 +518,30 @@ __global__ void k_scatter(const ac_cluster_problem* __restrict__ probs, int flag
 // CTA of a problem reduces the movement mean and clears `active` when
 // movement < tol.  mode 1 = segment mean into outs[p] (query reps).
 // ---------------------------------------------------------------------------
-constexpr int kUpdRows = 64;
+constexpr int kUpdRows = 32;    // rows per pipeline stage
+constexpr int kUpdStages = 4;   // row stages in flight
+constexpr int kUpdIdx = kUpdStages + 2;  // member-index slots (fetched two chunks ahead)
 
 AC_DEV void cp_async16(void* smem, const void* gmem) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
 AC_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-AC_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+template <int N>
+AC_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __host__ __device__ inline size_t update_smem_bytes(int d, int dtype) {
   const size_t rb = (size_t)d * (dtype == AC_DTYPE_BF16 ? 2 : 4);
-  return 2 * kUpdRows * ((rb + 15) / 16 * 16) + sizeof(float) * 2 * (size_t)d + 16;
+  return kUpdStages * kUpdRows * ((rb + 15) / 16 * 16) + sizeof(int) * kUpdIdx * kUpdRows +
+         sizeof(float) * 2 * (size_t)d + 16;
 }
 
+// One CTA per centre.  Member rows (stable label order) are gathered into a
+// 4-stage shared-memory ring with cp.async.  The member indices are
+// register-prefetched two chunks ahead, so neither the index load nor the
+// row load sits on the critical path.  Thread t < D owns the f64 chain of
+// dimension t and adds the members strictly in order (first row
+// initialises), exactly like np.add.reduceat(x[order].astype(f64), starts).
 __global__ void __launch_bounds__(256)
 k_update(const ac_cluster_problem* __restrict__ probs, int dtype, int d, double tol,
          int mode /*0 = lloyd update, 1 = segment mean into out*/, float* const* outs) {
@@ -530,58 +555,86 @@ k_update(const ac_cluster_problem* __restrict__ probs, int dtype, int d, double 
   const int esz = dtype == AC_DTYPE_BF16 ? 2 : 4;
   const int row_bytes = d * esz;
   const int rbp = (row_bytes + 15) / 16 * 16;
-  unsigned char* buf0 = usm;
-  unsigned char* buf1 = usm + (size_t)kUpdRows * rbp;
-  float* sq = reinterpret_cast<float*>(usm + 2 * (size_t)kUpdRows * rbp);
+  unsigned char* ring = usm;
+  int* pidx = reinterpret_cast<int*>(usm + (size_t)kUpdStages * kUpdRows * rbp);
+  float* sq = reinterpret_cast<float*>(pidx + kUpdIdx * kUpdRows);
   const int cnt = P.counts[c], s0 = P.starts[c];
   const char* xb = reinterpret_cast<const char*>(P.x);
-  const bool vec = (row_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(P.x) & 15) == 0);
+  const bool vec = (row_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(P.x) & 15) == 0) &&
+                   (row_bytes / 16 <= (int)blockDim.x);
   const int nchunks = (cnt + kUpdRows - 1) / kUpdRows;
+  // gather layout: `tpr` threads per row, each one 16-byte piece
+  const int tpr = vec ? row_bytes / 16 : 1;
+  const int rpp = blockDim.x / tpr;  // rows per pass
+  const int my_r = tid / tpr, my_part = tid - my_r * tpr;
 
-  auto issue = [&](int chunk, unsigned char* dst) {
-    const int m0 = chunk * kUpdRows;
-    const int rows = min(kUpdRows, cnt - m0);
-    if (vec) {
-      const int vpr = row_bytes / 16;
-      for (int e = tid; e < rows * vpr; e += blockDim.x) {
-        const int r = e / vpr, part = e - r * vpr;
-        const int64_t row = P.perm[s0 + m0 + r];
-        cp_async16(dst + (size_t)r * rbp + part * 16, xb + row * row_bytes + part * 16);
-      }
-    } else {
-      for (int e = tid; e < rows * d; e += blockDim.x) {
-        const int r = e / d, t = e - r * d;
-        const int64_t row = P.perm[s0 + m0 + r];
-        if (esz == 2)
-          reinterpret_cast<__nv_bfloat16*>(dst + (size_t)r * rbp)[t] =
-              reinterpret_cast<const __nv_bfloat16*>(P.x)[row * d + t];
-        else
-          reinterpret_cast<float*>(dst + (size_t)r * rbp)[t] =
-              reinterpret_cast<const float*>(P.x)[row * d + t];
+  auto fetch_idx = [&](int chunk) -> int {  // issue (do not wait for) one member index
+    const int m = chunk * kUpdRows + tid;
+    return (chunk < nchunks && tid < kUpdRows && m < cnt) ? P.perm[s0 + m] : 0;
+  };
+  auto put_idx = [&](int chunk, int v) {
+    if (tid < kUpdRows) pidx[(chunk % kUpdIdx) * kUpdRows + tid] = v;
+  };
+  auto issue_rows = [&](int chunk) {  // rows of `chunk` (indices already in smem)
+    if (chunk < nchunks) {
+      const int rows = min(kUpdRows, cnt - chunk * kUpdRows);
+      unsigned char* dst = ring + (size_t)(chunk % kUpdStages) * kUpdRows * rbp;
+      const int* idx = pidx + (chunk % kUpdIdx) * kUpdRows;
+      if (vec) {
+        for (int r = my_r; r < rows; r += rpp)
+          cp_async16(dst + (size_t)r * rbp + my_part * 16,
+                     xb + (int64_t)idx[r] * row_bytes + my_part * 16);
+      } else {
+        for (int e = tid; e < rows * d; e += blockDim.x) {
+          const int r = e / d, t = e - r * d;
+          const int64_t row = idx[r];
+          if (esz == 2)
+            reinterpret_cast<__nv_bfloat16*>(dst + (size_t)r * rbp)[t] =
+                reinterpret_cast<const __nv_bfloat16*>(P.x)[row * d + t];
+          else
+            reinterpret_cast<float*>(dst + (size_t)r * rbp)[t] =
+                reinterpret_cast<const float*>(P.x)[row * d + t];
+        }
       }
     }
-    cp_async_commit();
+    cp_async_commit();  // (possibly empty group: keeps the group count uniform)
   };
 
+  for (int ch = 0; ch < kUpdStages; ++ch) put_idx(ch, fetch_idx(ch));
+  int pf0 = fetch_idx(kUpdStages);      // in flight: consumed at iteration 0
+  int pf1 = fetch_idx(kUpdStages + 1);  // ... at iteration 1
+  __syncthreads();
+  for (int ch = 0; ch < kUpdStages - 1; ++ch) issue_rows(ch);
+
   double acc = 0.0;
-  if (nchunks > 0) issue(0, buf0);
   for (int j = 0; j < nchunks; ++j) {
-    unsigned char* cur = (j & 1) ? buf1 : buf0;
-    if (j + 1 < nchunks) issue(j + 1, (j & 1) ? buf0 : buf1);
-    else cp_async_commit();
-    cp_async_wait1();
+    put_idx(j + kUpdStages, pf0);
+    pf0 = pf1;
+    pf1 = fetch_idx(j + kUpdStages + 2);
+    issue_rows(j + kUpdStages - 1);
+    cp_async_wait<kUpdStages - 1>();
     __syncthreads();
     if (tid < d) {
+      // all loads of the chunk first, then the dependent f64 chain
       const int rows = min(kUpdRows, cnt - j * kUpdRows);
-      for (int r = 0; r < rows; ++r) {
-        const unsigned char* rp = cur + (size_t)r * rbp;
-        const float v = (esz == 2) ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rp)[tid])
-                                   : reinterpret_cast<const float*>(rp)[tid];
-        acc = (j == 0 && r == 0) ? (double)v : __dadd_rn(acc, (double)v);
+      const unsigned char* cur = ring + (size_t)(j % kUpdStages) * kUpdRows * rbp + (size_t)tid * esz;
+      float v[kUpdRows];
+#pragma unroll
+      for (int r = 0; r < kUpdRows; ++r) {
+        float f = 0.f;
+        if (r < rows)
+          f = (esz == 2) ? __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(cur + (size_t)r * rbp))
+                         : *reinterpret_cast<const float*>(cur + (size_t)r * rbp);
+        v[r] = f;
       }
+      if (j == 0) acc = (double)v[0];  // np.add.reduceat: the first member initialises
+#pragma unroll
+      for (int r = 0; r < kUpdRows; ++r)
+        if (r < rows && (j > 0 || r > 0)) acc = __dadd_rn(acc, (double)v[r]);
     }
     __syncthreads();
   }
+  cp_async_wait<0>();
   float* dst = (mode == 0) ? P.centers + (int64_t)c * d : outs[blockIdx.y] + (int64_t)c * d;
   if (tid < d) {
     const float nv = __double2float_rn(__ddiv_rn(acc, (double)cnt));
@@ -606,6 +659,154 @@ k_update(const ac_cluster_problem* __restrict__ probs, int dtype, int d, double 
       const volatile float* mv = P.movement;
       const float s = pw_sum<float>([&](int i) { return mv[i]; }, k);
       const float mean = __double2float_rn(__ddiv_rn((double)s, (double)k));
+      P.status[AC_ST_DONE] = 0;
+      P.status[AC_ST_NITER] += 1;
+      if ((double)mean < tol) P.status[AC_ST_ACTIVE] = 0;
+    }
+  }
+}
+
+// Warp-per-centre variant for d a multiple of 32 (the hot path: D = 64/128).
+// Lane l owns dimensions [l*DPL, l*DPL + DPL) — DPL independent f64 chains —
+// and walks the members in order.  Member rows are gathered by the warp
+// itself into a private 3-stage shared-memory ring (cp.async, 32 rows per
+// stage), so ~3 x 32 rows per centre are in flight while the current stage
+// is added; hundreds of centres run concurrently and the kernel is bound by
+// the gather bandwidth, not by the f64 add latency.
+constexpr int kUpdWRows = 32;
+constexpr int kUpdWStages = 3;
+constexpr int kUpdWarps = 4;  // centres per CTA
+
+inline size_t update_w_smem(int d, int dtype) {
+  const int esz = dtype == AC_DTYPE_BF16 ? 2 : 4;
+  return (size_t)kUpdWarps * kUpdWStages * kUpdWRows * d * esz + (size_t)kUpdWarps * 2 * d * 4;
+}
+
+template <int DPL, bool BF16>
+__global__ void __launch_bounds__(32 * kUpdWarps)
+k_update_w(const ac_cluster_problem* __restrict__ probs, int d, double tol, int mode,
+           float* const* outs) {
+  extern __shared__ __align__(16) unsigned char wsm[];
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  if (mode == 0 && P.status[AC_ST_ACTIVE] == 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * kUpdWarps + warp;
+  const int k = P.k;
+  if (c >= k) return;
+  constexpr int ESZ = BF16 ? 2 : 4;
+  const int row_bytes = d * ESZ;
+  const int stage_bytes = kUpdWRows * row_bytes;
+  unsigned char* ring = wsm + (size_t)warp * kUpdWStages * stage_bytes;
+  float* s_sq = reinterpret_cast<float*>(wsm + (size_t)kUpdWarps * kUpdWStages * stage_bytes) +
+                warp * 2 * d;
+  const int cnt = P.counts[c], s0 = P.starts[c];
+  const int32_t* perm = P.perm + s0;
+  const char* xb = reinterpret_cast<const char*>(P.x);
+  const int cpr = row_bytes / 16;        // 16-byte pieces per row
+  const int nb = (cnt + kUpdWRows - 1) / kUpdWRows;
+
+  // member indices are register-prefetched one stage ahead of their rows
+  auto fetch = [&](int b) -> int {
+    const int m = b * kUpdWRows + lane;
+    return (b < nb && m < cnt) ? perm[m] : 0;
+  };
+  int nxt = fetch(0);
+  auto issue = [&](int b) {
+    const int myidx = nxt;
+    nxt = fetch(b + 1);
+    if (b < nb) {
+      const int base = b * kUpdWRows;
+      const int rows = min(kUpdWRows, cnt - base);
+      unsigned char* dst = ring + (size_t)(b % kUpdWStages) * stage_bytes;
+      for (int e = lane; e < kUpdWRows * cpr; e += 32) {
+        const int r = e / cpr, part = e - r * cpr;
+        const int row = __shfl_sync(0xffffffffu, myidx, r);
+        if (r < rows) cp_async16(dst + r * row_bytes + part * 16, xb + (int64_t)row * row_bytes + part * 16);
+      }
+    }
+    cp_async_commit();
+  };
+
+  double acc[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) acc[i] = 0.0;
+  for (int b = 0; b < kUpdWStages - 1; ++b) issue(b);
+  for (int b = 0; b < nb; ++b) {
+    issue(b + kUpdWStages - 1);
+    cp_async_wait<kUpdWStages - 1>();
+    __syncwarp();
+    const unsigned char* cur = ring + (size_t)(b % kUpdWStages) * stage_bytes + lane * DPL * ESZ;
+    const int rows = min(kUpdWRows, cnt - b * kUpdWRows);
+    float v[kUpdWRows][DPL];
+#pragma unroll
+    for (int r = 0; r < kUpdWRows; ++r) {
+      const unsigned char* rp = cur + r * row_bytes;
+      if constexpr (BF16) {
+        if constexpr (DPL == 2) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(rp);
+          v[r][0] = __uint_as_float(w << 16); v[r][1] = __uint_as_float(w & 0xffff0000u);
+        } else {
+          const uint2 w = *reinterpret_cast<const uint2*>(rp);
+          v[r][0] = __uint_as_float(w.x << 16); v[r][1] = __uint_as_float(w.x & 0xffff0000u);
+          v[r][2] = __uint_as_float(w.y << 16); v[r][3] = __uint_as_float(w.y & 0xffff0000u);
+        }
+      } else {
+        if constexpr (DPL == 2) {
+          const float2 f = *reinterpret_cast<const float2*>(rp);
+          v[r][0] = f.x; v[r][1] = f.y;
+        } else {
+          const float4 f = *reinterpret_cast<const float4*>(rp);
+          v[r][0] = f.x; v[r][1] = f.y; v[r][2] = f.z; v[r][3] = f.w;
+        }
+      }
+    }
+    if (b == 0) {
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) acc[i] = (double)v[0][i];  // first member initialises
+    }
+    if (rows == kUpdWRows && b > 0) {
+#pragma unroll
+      for (int r = 0; r < kUpdWRows; ++r)
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) acc[i] = __dadd_rn(acc[i], (double)v[r][i]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < kUpdWRows; ++r) {
+        if (r >= rows) break;
+        if (b == 0 && r == 0) continue;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) acc[i] = __dadd_rn(acc[i], (double)v[r][i]);
+      }
+    }
+    __syncwarp();  // the stage is refilled by the next issue
+  }
+  cp_async_wait<0>();
+  float* dst = (mode == 0) ? P.centers + (int64_t)c * d : outs[blockIdx.y] + (int64_t)c * d;
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    const int t = lane * DPL + i;
+    const float nv = __double2float_rn(__ddiv_rn(acc[i], (double)cnt));
+    if (mode == 0) {
+      const float df = __fsub_rn(nv, dst[t]);
+      s_sq[t] = __fmul_rn(df, df);
+      s_sq[d + t] = __fmul_rn(nv, nv);
+    }
+    dst[t] = nv;
+  }
+  if (mode != 0) return;
+  __syncwarp();
+  if (lane == 0) {
+    const float* a = s_sq;
+    const float* bq = s_sq + d;
+    P.movement[c] = __fsqrt_rn(pw_sum<float>([&](int i) { return a[i]; }, d));
+    P.cc[c] = pw_sum<float>([&](int i) { return bq[i]; }, d);
+    __threadfence();
+    const int prev = atomicAdd(&P.status[AC_ST_DONE], 1);
+    if (prev == k - 1) {
+      __threadfence();
+      const volatile float* mv = P.movement;
+      const float sm = pw_sum<float>([&](int i) { return mv[i]; }, k);
+      const float mean = __double2float_rn(__ddiv_rn((double)sm, (double)k));
       P.status[AC_ST_DONE] = 0;
       P.status[AC_ST_NITER] += 1;
       if ((double)mean < tol) P.status[AC_ST_ACTIVE] = 0;
@@ -940,7 +1141,11 @@ extern "C" int ac_row_sqnorm(const void* x, int dtype, int64_t rows, int d, floa
                              void* stream) {
   if (rows < 0 || d < 1) { ac_host::set_error("ac_row_sqnorm: bad shape"); return AC_ERR_DIM; }
   if (rows == 0) return AC_OK;
-  k_row_sqnorm<<<(unsigned)((rows + 255) / 256), 256, 0, S(stream)>>>(x, dtype, rows, d, out);
+  const size_t smem = sizeof(float) * kNormRows * (d + 1);
+  int rc = set_smem((const void*)k_row_sqnorm, smem);
+  if (rc) return rc;
+  k_row_sqnorm<<<(unsigned)((rows + kNormRows - 1) / kNormRows), kNormRows, smem, S(stream)>>>(
+      x, dtype, rows, d, out);
   AC_CHECK_LAUNCH("k_row_sqnorm");
   return AC_OK;
 }
@@ -949,8 +1154,11 @@ extern "C" int ac_l2norm(const void* x, int dtype, int64_t rows, int d, float* o
                          float* out_sq, uint8_t* degenerate, void* stream) {
   if (rows < 0 || d < 1) { ac_host::set_error("ac_l2norm: bad shape"); return AC_ERR_DIM; }
   if (rows == 0) return AC_OK;
-  k_l2norm<<<(unsigned)((rows + 127) / 128), 128, 0, S(stream)>>>(x, dtype, rows, d, out, out_sq,
-                                                                   degenerate);
+  const size_t smem = sizeof(float) * kNormRows * (d + 1);
+  int rc = set_smem((const void*)k_l2norm, smem);
+  if (rc) return rc;
+  k_l2norm<<<(unsigned)((rows + kNormRows - 1) / kNormRows), kNormRows, smem, S(stream)>>>(
+      x, dtype, rows, d, out, out_sq, degenerate);
   AC_CHECK_LAUNCH("k_l2norm");
   return AC_OK;
 }
@@ -959,7 +1167,11 @@ extern "C" int ac_lloyd_prepare(const ac_cluster_problem* probs, int nprob, int 
                                 int64_t max_n, int max_k, void* stream) {
   if (nprob <= 0) return AC_OK;
   k_status_init<<<(nprob + 127) / 128, 128, 0, S(stream)>>>(probs, nprob);
-  k_problem_xx<<<dim3((unsigned)((max_n + 255) / 256), nprob), 256, 0, S(stream)>>>(probs, dtype, d);
+  const size_t xsm = sizeof(float) * kNormRows * (d + 1);
+  int rc = set_smem((const void*)k_problem_xx, xsm);
+  if (rc) return rc;
+  k_problem_xx<<<dim3((unsigned)((max_n + kNormRows - 1) / kNormRows), nprob), kNormRows, xsm,
+                 S(stream)>>>(probs, dtype, d);
   k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, S(stream)>>>(probs, d, 0);
   AC_CHECK_LAUNCH("ac_lloyd_prepare");
   return AC_OK;
@@ -1047,10 +1259,28 @@ extern "C" int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dt
 static int update_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d, int max_k,
                        double tol, int mode, float* const* outs, cudaStream_t st) {
   if (d > 256) { ac_host::set_error("update: d=%d > 256", d); return AC_ERR_DIM; }
+  if (d % 32 == 0 && (d == 64 || d == 128)) {
+    const dim3 grid((unsigned)((max_k + kUpdWarps - 1) / kUpdWarps), nprob);
+    const bool bf = dtype == AC_DTYPE_BF16;
+    const size_t wsmem = update_w_smem(d, dtype);
+    const void* fn = d == 64 ? (bf ? (const void*)k_update_w<2, true> : (const void*)k_update_w<2, false>)
+                             : (bf ? (const void*)k_update_w<4, true> : (const void*)k_update_w<4, false>);
+    int rc = set_smem(fn, wsmem);
+    if (rc) return rc;
+    if (d == 64) {
+      if (bf) k_update_w<2, true><<<grid, 32 * kUpdWarps, wsmem, st>>>(probs, d, tol, mode, outs);
+      else k_update_w<2, false><<<grid, 32 * kUpdWarps, wsmem, st>>>(probs, d, tol, mode, outs);
+    } else {
+      if (bf) k_update_w<4, true><<<grid, 32 * kUpdWarps, wsmem, st>>>(probs, d, tol, mode, outs);
+      else k_update_w<4, false><<<grid, 32 * kUpdWarps, wsmem, st>>>(probs, d, tol, mode, outs);
+    }
+    AC_CHECK_LAUNCH("k_update_w");
+    return AC_OK;
+  }
   const size_t smem = update_smem_bytes(d, dtype);
   int rc = set_smem((const void*)k_update, smem);
   if (rc) return rc;
-  k_update<<<dim3(max_k, nprob), 256, smem, st>>>(probs, dtype, d, tol, mode, outs);
+  k_update<<<dim3(max_k, nprob), d <= 128 ? 128 : 256, smem, st>>>(probs, dtype, d, tol, mode, outs);
   AC_CHECK_LAUNCH("k_update");
   return AC_OK;
 }

@@ -172,9 +172,26 @@ class Batch:
         L.call("ac_kmeanspp", self.dev.data_ptr(), self.P, self.dtype, self.D, self.max_n, max_k,
                draws.data_ptr(), L.stream_ptr())
 
-    def lloyd(self, max_iter: int, tol: float, poll_every: int = 0):
-        L.call("ac_lloyd", *self.args(), int(max_iter), float(tol), int(poll_every),
-               self.desc.ctypes.data, L.stream_ptr())
+    def lloyd(self, max_iter: int, tol: float, poll_every: int = 0, group: int = 0):
+        """Lloyd on every problem; ``group`` > 0 runs the problems in blocks of
+        that many, so a block's points stay resident in the 126 MB L2 across
+        its iterations (each assign/update pass then reads L2, not HBM)."""
+        if group <= 0 or group >= self.P:
+            L.call("ac_lloyd", *self.args(), int(max_iter), float(tol), int(poll_every),
+                   self.desc.ctypes.data, L.stream_ptr())
+            return
+        isz = self.desc.dtype.itemsize
+        for g0 in range(0, self.P, group):
+            g1 = min(self.P, g0 + group)
+            L.call("ac_lloyd", self.dev.data_ptr() + g0 * isz, g1 - g0, self.dtype, self.D,
+                   max(self.ns[g0:g1]), max(self.kcaps[g0:g1]), int(max_iter), float(tol),
+                   int(poll_every), self.desc.ctypes.data + g0 * isz, L.stream_ptr())
+
+    def l2_group(self, budget: float = 48e6) -> int:
+        """Problems per block so that a block's points fit in ~`budget` bytes of L2."""
+        esz = 2 if self.dtype == L.DTYPE_BF16 else 4
+        per = max(1, max(self.ns) * self.D * esz)
+        return max(1, int(budget // per))
 
     def prepare(self):
         L.call("ac_lloyd_prepare", *self.args(), L.stream_ptr())

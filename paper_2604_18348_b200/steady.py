@@ -139,29 +139,42 @@ class SteadyStep:
         # CUDA events recorded inside the graph around the attention kernel
         # and around the clustering (kernel time of the last replay)
         self.ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
+        self.side = torch.cuda.Stream()
+        self.fork = torch.cuda.Event()
+        self.join = torch.cuda.Event()
 
     # ------------------------------------------------------------------
     def _enqueue(self):
-        """Every kernel of one warm step, in order, on the current stream."""
+        """Every kernel of one warm step.  The key side (Lloyd, envelopes,
+        K/V permutation) and the query side (normalise, Lloyd, reps) are
+        independent until selection, so they run on two streams; both are
+        latency-bound chains that leave most SMs idle on their own."""
         H, Ln, D = self.H, self.L, self.D
         p = self.p
-        s = L.stream_ptr()
         kb, qb = self.kb, self.qb
+        main = torch.cuda.current_stream()
         self.ev[0].record()
-        L.call("ac_lloyd", *kb.args(), int(p.max_iter), float(p.tol), 0, kb.desc.ctypes.data, s)
+        self.fork.record(main)
+        self.side.wait_event(self.fork)
+        with torch.cuda.stream(self.side):
+            s = L.stream_ptr()
+            kb.lloyd(p.max_iter, p.tol)
+            L.call("ac_envelopes", self.env_desc.data_ptr(), H, self.dt, D, kb.max_k,
+                   self.pmax.data_ptr(), self.pmin.data_ptr(), s)
+            L.call("ac_permute_rows_heads", self.K.data_ptr(), self.dt, D, self.kperm.data_ptr(),
+                   Ln, H, self.kp.data_ptr(), s)
+            L.call("ac_permute_rows_heads", self.V.data_ptr(), self.dt, D, self.kperm.data_ptr(),
+                   Ln, H, self.vp.data_ptr(), s)
+            self.join.record(self.side)
+        s = L.stream_ptr()
         L.call("ac_l2norm", self.Q.data_ptr(), self.dt, H * Ln, D, self.qn.data_ptr(), 0,
                self.qdeg.data_ptr(), s)
-        L.call("ac_lloyd", *qb.args(), int(p.max_iter), float(p.tol), 0, qb.desc.ctypes.data, s)
+        qb.lloyd(p.max_iter, p.tol)
         L.call("ac_segment_mean", self.reps_desc.data_ptr(), H, L.DTYPE_F32, D, self.gq,
                self.reps_ptrs.data_ptr(), s)
-        L.call("ac_envelopes", self.env_desc.data_ptr(), H, self.dt, D, kb.max_k,
-               self.pmax.data_ptr(), self.pmin.data_ptr(), s)
+        main.wait_event(self.join)
         L.call("ac_select", self.sel_desc.data_ptr(), H, D, self.scorer, self.gq, kb.max_k,
                self.stride, s)
-        L.call("ac_permute_rows_heads", self.K.data_ptr(), self.dt, D, self.kperm.data_ptr(), Ln, H,
-               self.kp.data_ptr(), s)
-        L.call("ac_permute_rows_heads", self.V.data_ptr(), self.dt, D, self.kperm.data_ptr(), Ln, H,
-               self.vp.data_ptr(), s)
         L.call("ac_build_q_layout", self.Q.data_ptr(), self.dt, D, Ln, H, self.qperm.data_ptr(),
                self.qstarts.data_ptr(), self.qcounts.data_ptr(), self.qlab.data_ptr(),
                self.gq_t.data_ptr(), self.gq, self.nruns.data_ptr(), self.stride,
