@@ -88,6 +88,9 @@ typedef struct ac_cluster_problem {
   const int32_t* plan_n;/* pairwise-sum plan of length n (ac_pw_plan_build)   */
   const int32_t* plan_k;/* pairwise-sum plan of length k                      */
   double* dscratch;     /* [n] f64 scratch (k-means++ cdf, tau)               */
+  void* planes;         /* optional, f32 points only: [3][n][d] bf16 hi/mid/lo
+                           split of x (written by ac_lloyd_prepare); enables
+                           the tensor-core assignment for f32 points           */
   int64_t n;
   int32_t k;
   int32_t order;        /* AC_ORDER_* of the reference's x @ centres.T        */

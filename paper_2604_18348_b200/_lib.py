@@ -32,7 +32,8 @@ PROBLEM_DTYPE = np.dtype([
     ("x", "u8"), ("xx", "u8"), ("centers", "u8"), ("cc", "u8"), ("labels", "u8"),
     ("best", "u8"), ("counts", "u8"), ("perm", "u8"), ("starts", "u8"), ("tile_hist", "u8"),
     ("inertia", "u8"), ("movement", "u8"), ("status", "u8"), ("plan_n", "u8"),
-    ("plan_k", "u8"), ("dscratch", "u8"), ("n", "i8"), ("k", "i4"), ("order", "i4"),
+    ("plan_k", "u8"), ("dscratch", "u8"), ("planes", "u8"), ("n", "i8"), ("k", "i4"),
+    ("order", "i4"),
 ])
 SELECT_DTYPE = np.dtype([
     ("reps", "u8"), ("emax", "u8"), ("emin", "u8"), ("counts", "u8"), ("kstarts", "u8"),

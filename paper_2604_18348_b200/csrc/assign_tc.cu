@@ -7,32 +7,31 @@
 // Labels must be bit-identical (Lloyd is not converged at max_iter, so one
 // flipped near-tie cascades — SURVEY.md §7 hard part 1).  Design:
 //
-//   1. x·c on tcgen05 (kind::f16, f32 accumulation in TMEM).  Centres are
-//      split into three bf16 planes c = hi + mid + lo (exact for f32);
-//      bf16 points are one exact plane (3 MMAs per K step), f32 points are
-//      split the same way in shared memory (6 MMAs: every plane product
-//      down to 2^-16 relative).
-//   2. Epilogue, one thread per row (= TMEM lane): approximate d~_c, its
-//      minimum, and every centre with d~_c <= min + 2T is a candidate, where
-//      T bounds |d~ - d_ref| rigorously (split + accumulation error and the
-//      reference chain's own rounding, both <= c·u·||x||·||c||).
+//   1. e_c = ||c||^2 - 2 x·c on tcgen05 (kind::f16, f32 accumulation in
+//      TMEM).  Centres enter as three bf16 planes of -2c (exact split of
+//      f32), ||c||^2 as a 3-way split picked up by one extra K=16 MMA against
+//      a constant ones block; bf16 points are one exact plane (1 + 3 MMA
+//      groups per tile), f32 points arrive as their exact hi/mid/lo bf16
+//      planes (written once per Lloyd run by ac_lloyd_prepare; 1 + 6 groups,
+//      every plane product down to 2^-16 relative).
+//   2. Epilogue, one thread per row (= TMEM lane): e_min and the candidate
+//      mask e_c <= d~_min + 2T - ||x||^2 straight from TMEM, where T bounds
+//      |d~ - d_ref| rigorously (split + accumulation error and the reference
+//      chain's own rounding, both <= c·u·(||x||·||c|| + ||c||^2)).
 //   3. Candidates are recomputed with the reference's exact sequential
-//      fmaf chain (x and c reconstructed exactly from the bf16 planes in
-//      shared memory) and the first-index minimum of the exact values wins.
-//      Almost every row has one candidate — its exact d is what `best`
-//      (inertia, repair, stage MSE) needs anyway.
+//      fmaf chain (x and c reconstructed exactly from shared memory) and the
+//      first-index minimum of the exact values wins.  Almost every row has
+//      one candidate — its exact d is what `best` (inertia, repair, stage
+//      MSE) needs anyway; a warp's extra candidates are spread over its lanes.
 //
 // So labels and distances equal k_assign_seq's (the all-FFMA kernel) bit
-// for bit; tests/test_gpu_parity.py checks exactly that.
+// for bit; tests/test_assign_tc.py checks exactly that, on adversarial ties.
 //
-// Warp roles (448 threads, one CTA per SM, persistent over the tiles of a
+// Warp roles (320 threads, one CTA per SM, persistent over the tiles of a
 // batch of problems):
-//   warp 0      TMA producer: 128-row x tiles (f32: two 32-column SW128
-//               boxes; bf16: one 64-column box) into a ring
+//   warp 0      TMA producer: 128-row x tiles (1 or 3 planes) into a ring
 //   warp 1      MMA issuer (single thread), TMEM owner (2 x 128 columns)
-//   warps 2-5   f32 input only: split x into hi/mid/lo bf16 planes (SW128
-//               K-major, the canonical UMMA layout)
-//   warps 6-13  two epilogue warpgroups, alternating tiles (one TMEM
+//   warps 2-9   two epilogue warpgroups, alternating tiles (one TMEM
 //               accumulator each): argmin, exact fix-up, labels / best /
 //               per-tile label histogram (the tiling matches k_scatter).
 // Compiled with --fmad=false: the fix-up reproduces numpy's unfused ops.
@@ -52,24 +51,27 @@ constexpr int BM = 128;     // rows per tile (== kAsgBM: shared tiling with the 
 constexpr int DIM = 64;     // head_dim handled by this kernel
 constexpr int NBMAX = 128;  // centres per problem per launch (k - c_lo)
 constexpr int MAXP = 32;    // problems per launch (tensor maps travel as kernel params)
-constexpr int THREADS = 448;
-constexpr int W_TMA = 0, W_MMA = 1, W_CONV0 = 2, W_EPI0 = 6;
-constexpr int XF_BYTES = BM * DIM * 4;  // f32 tile: two 16 KB SW128 boxes of 32 columns
+constexpr int THREADS = 320;
+constexpr int W_TMA = 0, W_MMA = 1, W_EPI0 = 2;
 constexpr int PL_BYTES = BM * DIM * 2;  // one bf16 plane of a tile (16 KB)
 constexpr int CF_STRIDE = DIM + 4;      // f32 centre rows, padded against bank conflicts
-constexpr int NBAR = 16;
-constexpr int QCAP = 64;  // per-warp queue of extra (row, centre) fix-up candidates
+constexpr int QCAP = 64;                // per-warp queue of extra (row, centre) fix-up candidates
 constexpr int SMEM_MAX = 227 * 1024;
+constexpr float kPadE = 3.0e38f;        // e of the padding columns (never a candidate)
 
 // Shared-memory layout, sized per launch from the largest centre count
-// (cap = max round16(k - c_lo)).  f32 points: x stages (1 or 2) of 32 KB +
-// 2 x 3 split planes; bf16 points: 4 x 16 KB x stages (the MMA operand).
-// Then the centre planes [3][cap][64] bf16 (SW128), the exact f32 centres
-// [cap][68], ||c||^2 [128], two label histograms [2][128], the epilogue
-// warps' fix-up queues [8][64] x (entry, result), barriers.
+// (cap = max round16(k - c_lo)):
+//   x stages   XS x NP planes x [128 rows][64] bf16 (SW128, TMA-written);
+//              NP = 1 for bf16 points (exact), 3 for f32 points (hi/mid/lo)
+//   centres    3 planes of -2c [cap][64] bf16 (SW128)
+//   aug        A: [128][64] bf16 with columns 0..2 = 1;  B: [cap][64] with
+//              columns 0..2 = the exact 3-way split of ||c||^2  -> one extra
+//              K=16 MMA adds ||c||^2, so TMEM holds e_c = ||c||^2 - 2 x.c
+//   exact      f32 centres [cap][68], ||c||^2 [128]
+//   epilogue   two label histograms [2][128], fix-up queues [8][64] x 2 words
 struct Layout {
-  int xs, xstride, off_xp, off_cp, cp_bytes, off_cf, off_cc, off_hist, off_q, off_bar, off_misc,
-      smem;
+  int np, xs, stage_bytes, off_cp, cp_bytes, off_aa, off_ab, off_cf, off_cc, off_hist, off_q,
+      off_bar, off_misc, smem;
 };
 
 struct Params {
@@ -82,29 +84,25 @@ struct Params {
   Layout lay;
 };
 
-__host__ __device__ inline Layout make_layout(int dtype, int cap) {
+__host__ __device__ inline Layout make_layout(int dtype, int cap, int xs) {
   Layout l;
-  const bool f32 = dtype == AC_DTYPE_F32;
-  l.xs = f32 ? (cap <= 80 ? 2 : 1) : 4;
-  l.xstride = f32 ? XF_BYTES : PL_BYTES;
-  l.off_xp = l.xs * l.xstride;
-  l.off_cp = l.off_xp + (f32 ? 2 * 3 * PL_BYTES : 0);
+  l.np = dtype == AC_DTYPE_F32 ? 3 : 1;
+  l.xs = xs;
+  l.stage_bytes = l.np * PL_BYTES;
+  l.off_cp = l.xs * l.stage_bytes;
   l.cp_bytes = cap * 128;
-  l.off_cf = l.off_cp + 3 * l.cp_bytes;
+  l.off_aa = l.off_cp + 3 * l.cp_bytes;
+  l.off_ab = l.off_aa + BM * 128;
+  l.off_cf = l.off_ab + l.cp_bytes;
   l.off_cc = l.off_cf + cap * CF_STRIDE * 4;
   l.off_hist = l.off_cc + NBMAX * 4;
   l.off_q = l.off_hist + 2 * NBMAX * 4;
   l.off_bar = l.off_q + 8 * QCAP * 8;
-  l.off_misc = l.off_bar + NBAR * 8;
+  l.off_misc = l.off_bar + 16 * 8;
   l.smem = l.off_misc + 64 + 1024;  // + alignment slack
   return l;
 }
 
-// 1 KB-aligned view of dynamic shared memory (offset arithmetic on the
-// shared pointer itself, so the compiler keeps shared-space accesses)
-AC_DEV unsigned char* align1024(unsigned char* p) {
-  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
-}
 // byte offset of 16-byte chunk j of row r in a 128-byte-row SW128 tile
 AC_DEV int sw128(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
 
@@ -144,8 +142,7 @@ AC_DEV void join8(const uint4& h, const uint4& m, const uint4& l, float (&v)[8])
 
 // the reference's d for row r of the x tile and f32 centre row cf:
 // sequential fmaf chain from 0 (OpenBLAS general path), then sq_dist.
-// x comes from shared memory: the three split planes (f32 points, joined
-// exactly) or the bf16 tile itself.
+// x comes from the tile's planes in shared memory (exactly joined).
 AC_DEV float exact_dist(const unsigned char* xsm, bool f32in, int r, const float* cf, float xx,
                         float cc) {
   float acc = 0.f;
@@ -175,29 +172,38 @@ AC_DEV float exact_dist(const unsigned char* xsm, bool f32in, int r, const float
   return sq_dist(xx, acc, cc);
 }
 
+AC_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
 k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __restrict__ probs) {
   extern __shared__ __align__(1024) unsigned char smraw[];
-  unsigned char* sm = align1024(smraw);
+  unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool f32in = prm.dtype == AC_DTYPE_F32;
   const Layout& lay = prm.lay;
-  const int XS = lay.xs;
+  const int XS = lay.xs, NP = lay.np, SB = lay.stage_bytes, CPB = lay.cp_bytes;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + lay.off_bar);
-  uint64_t* xfull = bars;       // [4] TMA -> converter (f32) / MMA (bf16)
-  uint64_t* xempty = bars + 4;  // [4] converter (f32) / epilogue (bf16) -> TMA
-  uint64_t* pfull = bars + 8;   // [2] converter -> MMA
-  uint64_t* pempty = bars + 10; // [2] epilogue -> converter
-  uint64_t* afull = bars + 12;  // [2] MMA commit -> epilogue
-  uint64_t* aempty = bars + 14; // [2] epilogue -> MMA
+  uint64_t* xfull = bars;        // [4] TMA -> MMA
+  uint64_t* xempty = bars + 4;   // [4] epilogue -> TMA
+  uint64_t* afull = bars + 8;    // [2] MMA commit -> epilogue
+  uint64_t* aempty = bars + 10;  // [2] epilogue -> MMA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + lay.off_misc);
   int* s_ccmax = reinterpret_cast<int*>(sm + lay.off_misc + 16);
   float* s_cc = reinterpret_cast<float*>(sm + lay.off_cc);
   int* s_hist = reinterpret_cast<int*>(sm + lay.off_hist);
   unsigned char* cplanes = sm + lay.off_cp;
+  unsigned char* aug_a = sm + lay.off_aa;
+  unsigned char* aug_b = sm + lay.off_ab;
   float* cf32 = reinterpret_cast<float*>(sm + lay.off_cf);
-  const int CPB = lay.cp_bytes;
 
   if (tid == 0) {
     for (int s = 0; s < 4; ++s) {
@@ -205,14 +211,20 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       mbar_init(xempty + s, 128);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(pfull + b, 128);
-      mbar_init(pempty + b, 128);
       mbar_init(afull + b, 1);
       mbar_init(aempty + b, 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  // aug A: rows of (1, 1, 1, 0, ...): picks up the 3-way split of ||c||^2
+  for (int e = tid; e < BM * 8; e += THREADS) {
+    const int r = e >> 3, j = e & 7;
+    uint4 w = make_uint4(0u, 0u, 0u, 0u);
+    if (j == 0) w = make_uint4(0x3f803f80u, 0x00003f80u, 0u, 0u);  // bf16 1.0 = 0x3f80
+    *reinterpret_cast<uint4*>(aug_a + sw128(r, j)) = w;
+  }
   if (warp == W_MMA) tmem_alloc(tmem_slot, 256);
+  fence_proxy_async();
   fence_before();
   __syncthreads();
   fence_after();
@@ -239,8 +251,8 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
     const int ntiles_p = prm.tile0[p + 1] - ptile0;
     const int T = seg_end - t;
 
-    // ---- centres of this problem: bf16 planes (MMA), exact f32 rows
-    //      (fix-up), ||c||^2 (+inf past nb, masking the pad columns) ----
+    // ---- centres of this problem: -2c planes and ||c||^2 split (MMA),
+    //      exact f32 rows and ||c||^2 (fix-up) ----
     if (tid == 0) *s_ccmax = 0;
     __syncthreads();
     for (int e = tid; e < nbp * 8; e += THREADS) {
@@ -249,11 +261,11 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       if (c < nb) {
         const float4* src = reinterpret_cast<const float4*>(P.centers + (int64_t)(c_lo + c) * DIM + 8 * j);
         const float4 a = src[0], b = src[1];
-        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
         float4* dst = reinterpret_cast<float4*>(cf32 + c * CF_STRIDE + 8 * j);
         dst[0] = a;
         dst[1] = b;
+        v[0] = -2.f * a.x; v[1] = -2.f * a.y; v[2] = -2.f * a.z; v[3] = -2.f * a.w;
+        v[4] = -2.f * b.x; v[5] = -2.f * b.y; v[6] = -2.f * b.z; v[7] = -2.f * b.w;
       } else {
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = 0.f;
@@ -269,6 +281,19 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       const float cc = (c < nb) ? P.cc[c_lo + c] : INFINITY;
       s_cc[c] = cc;
       if (c < nb && cc > 0.f) atomicMax(s_ccmax, __float_as_int(cc));
+      if (c < nbp) {
+        // ||c||^2 split into columns 0..2 of the aug B row; padding rows get
+        // a huge e so that they are never a minimum or a candidate
+        const float v0 = (c < nb) ? cc : kPadE;
+        const __nv_bfloat16 h0 = __float2bfloat16_rn(v0);
+        const float r1 = __fsub_rn(v0, __bfloat162float(h0));
+        const __nv_bfloat16 h1 = __float2bfloat16_rn(r1);
+        const __nv_bfloat16 h2 = __float2bfloat16_rn(__fsub_rn(r1, __bfloat162float(h1)));
+        const uint32_t w0 = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+        const uint32_t w1 = (uint32_t)__bfloat16_as_ushort(h2);
+        *reinterpret_cast<uint4*>(aug_b + sw128(c, 0)) = make_uint4(w0, w1, 0u, 0u);
+        for (int j = 1; j < 8; ++j) *reinterpret_cast<uint4*>(aug_b + sw128(c, j)) = make_uint4(0u, 0u, 0u, 0u);
+      }
     }
     fence_proxy_async();  // generic-proxy smem writes -> tensor-core (async proxy) reads
     __syncthreads();
@@ -282,15 +307,10 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
           const int g = g0 + i, s = g % XS;
           if (g >= XS) mbar_wait_sleep(xempty + s, ((g / XS) - 1) & 1, 20);
           const int row = (t + i - ptile0) * BM;
-          unsigned char* dst = sm + s * lay.xstride;
-          if (f32in) {
-            mbar_expect_tx(xfull + s, XF_BYTES);
-            tma_load_2d(dst, &prm.x[p], 0, row, xfull + s);
-            tma_load_2d(dst + XF_BYTES / 2, &prm.x[p], 32, row, xfull + s);
-          } else {
-            mbar_expect_tx(xfull + s, PL_BYTES);
-            tma_load_2d(dst, &prm.x[p], 0, row, xfull + s);
-          }
+          unsigned char* dst = sm + s * SB;
+          mbar_expect_tx(xfull + s, SB);
+          for (int q = 0; q < NP; ++q)
+            tma_load_2d(dst + q * PL_BYTES, &prm.x[p], 0, (int)(q * n) + row, xfull + s);
         }
       }
       __syncwarp();
@@ -299,6 +319,7 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       if (lane == 0) {
         const uint32_t idesc = idesc_bf16(BM, nbp, false);
         const uint32_t ca = smem_u32(cplanes);
+        const uint32_t aa = smem_u32(aug_a), ab = smem_u32(aug_b);
         // plane products kept: (x plane, c plane), the x-hi terms first (bf16
         // points are exact in plane 0, so they use only those three); the
         // dropped terms are < 2^-23 relative
@@ -307,13 +328,13 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const int nterm = f32in ? 6 : 3;
         for (int i = 0; i < T; ++i) {
           const int g = g0 + i, s = g % XS, b = g & 1;
-          if (f32in) mbar_wait_sleep(pfull + b, (g >> 1) & 1, 21);
-          else mbar_wait_sleep(xfull + s, (g / XS) & 1, 22);
+          mbar_wait_sleep(xfull + s, (g / XS) & 1, 22);
           if (g >= 2) mbar_wait_sleep(aempty + b, ((g >> 1) - 1) & 1, 23);
           fence_after();
-          const uint32_t xa = f32in ? smem_u32(sm + lay.off_xp + b * 3 * PL_BYTES)
-                                    : smem_u32(sm + s * PL_BYTES);
+          const uint32_t xa = smem_u32(sm + s * SB);
           const uint32_t d = tmem + (uint32_t)(b * 128);
+          // ||c||^2 first (one K=16 step of the aug operands), then -2 x.c
+          umma_f16(d, sdesc(aa, 16, 1024), sdesc(ab, 16, 1024), idesc, 0u);
 #pragma unroll
           for (int term = 0; term < 6; ++term) {
             if (term >= nterm) break;
@@ -321,51 +342,26 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
             for (int kk = 0; kk < DIM / 16; ++kk) {
               const uint64_t ad = sdesc(xa + xi[term] * PL_BYTES + kk * 32, 16, 1024);
               const uint64_t bd = sdesc(ca + ci[term] * CPB + kk * 32, 16, 1024);
-              umma_f16(d, ad, bd, idesc, (term > 0 || kk > 0) ? 1u : 0u);
+              umma_f16(d, ad, bd, idesc, 1u);
             }
           }
           umma_commit(afull + b);
         }
       }
       __syncwarp();
-    } else if (warp < W_EPI0) {
-      // -------------------- f32 points: split into bf16 planes --------------------
-      if (f32in) {
-        const int r = tid - W_CONV0 * 32;  // 0..127
-        for (int i = 0; i < T; ++i) {
-          const int g = g0 + i, s = g % XS, b = g & 1;
-          mbar_wait_sleep(xfull + s, (g / XS) & 1, 24);
-          if (g >= 2) mbar_wait_sleep(pempty + b, ((g >> 1) - 1) & 1, 25);
-          const unsigned char* xs = sm + s * XF_BYTES;
-          unsigned char* xp = sm + lay.off_xp + b * 3 * PL_BYTES;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const unsigned char* box = xs + (j >> 2) * (XF_BYTES / 2);
-            const int q0 = (2 * j) & 7;
-            const float4 a = *reinterpret_cast<const float4*>(box + sw128(r, q0));
-            const float4 c = *reinterpret_cast<const float4*>(box + sw128(r, q0 + 1));
-            const float v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-            uint4 h, m, l;
-            split8(v, h, m, l);
-            const int off = sw128(r, j);
-            *reinterpret_cast<uint4*>(xp + off) = h;
-            *reinterpret_cast<uint4*>(xp + PL_BYTES + off) = m;
-            *reinterpret_cast<uint4*>(xp + 2 * PL_BYTES + off) = l;
-          }
-          mbar_arrive(xempty + s);
-          fence_proxy_async();
-          mbar_arrive(pfull + b);
-        }
-      }
     } else {
       // ------------------------------ epilogue ------------------------------
-      // e_c = cc - 2 acc ~ d~_c - ||x||^2; candidates: max(xx + e_c, 0) <=
-      // d~_min + 2T  <=>  e_c <= d~_min + 2T - xx (slack 0.5T for roundings)
+      // TMEM holds e_c ~ ||c||^2 - 2 x.c = d~_c - ||x||^2.  Candidates:
+      // max(xx + e_c, 0) <= d~_min + 2T  <=>  e_c <= d~_min + 2T - xx
+      // (slack 0.5T for the roundings of the comparison itself)
       const int wg = (warp - W_EPI0) >> 2;
       const int q = warp & 3;  // TMEM lane quarter this warp may access
       const int r = q * 32 + lane;
       const uint32_t lane_base = (uint32_t)(q * 32) << 16;
       int* hist = s_hist + wg * NBMAX;
+      uint32_t* qe = reinterpret_cast<uint32_t*>(sm + lay.off_q) + (warp - W_EPI0) * 2 * QCAP;
+      float* qr = reinterpret_cast<float*>(qe + QCAP);
+      const int nch = nbp >> 4;  // 16-column chunks
       int fixups = 0, wide = 0;
       for (int i = 0; i < T; ++i) {
         const int g = g0 + i;
@@ -375,38 +371,39 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const int64_t row = (int64_t)tile * BM + r;
         const bool valid = row < n;
         const float xx = valid ? P.xx[row] : 0.f;
-        const float tb = 0x1p-15f * sqrtf(xx) * cmax + 0x1p-20f * (xx + ccmax) + 1e-30f;
+        const float tb = 0x1p-15f * sqrtf(xx) * cmax + 0x1p-17f * (xx + ccmax) + 1e-30f;
         mbar_wait_sleep(afull + b, (g >> 1) & 1, 26);
         fence_after();
         const uint32_t acc_col = tmem + lane_base + (uint32_t)(b * 128);
-        float emin = INFINITY;
-        for (int c0 = 0; c0 < nbp; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(acc_col + c0, v);
+        float m4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        for (int ch = 0; ch < nch; ++ch) {
+          uint32_t v[16];
+          tmem_ld16(acc_col + ch * 16, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int u = 0; u < 32; ++u)
-            emin = fminf(emin, __fmaf_rn(-2.f, __uint_as_float(v[u]), s_cc[c0 + u]));
+          for (int u = 0; u < 16; u += 4)
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+              m4[a + 2 * (u >> 3)] = fminf(m4[a + 2 * (u >> 3)],
+                                           fminf(__uint_as_float(v[u + 2 * a]), __uint_as_float(v[u + 2 * a + 1])));
         }
+        const float emin = fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3]));
         const float dmin = fmaxf(xx + emin, 0.f);
         const float ethr = (dmin + 2.5f * tb) - xx;
         int c1 = INT_MAX, ncand = 0;
-        uint32_t mk[NBMAX / 32];
+        uint32_t mk[NBMAX / 32] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int ch = 0; ch < NBMAX / 32; ++ch) {
-          mk[ch] = 0u;
-          const int c0 = ch * 32;
-          if (c0 >= nbp) continue;
-          uint32_t v[32];
-          tmem_ld32(acc_col + c0, v);
+        for (int ch = 0; ch < NBMAX / 16; ++ch) {
+          if (ch >= nch) break;
+          uint32_t v[16];
+          tmem_ld16(acc_col + ch * 16, v);
           tmem_wait_ld();
           uint32_t m = 0;
 #pragma unroll
-          for (int u = 0; u < 32; ++u)
-            m |= (__fmaf_rn(-2.f, __uint_as_float(v[u]), s_cc[c0 + u]) <= ethr) ? (1u << u) : 0u;
-          mk[ch] = m;
+          for (int u = 0; u < 16; ++u) m |= (__uint_as_float(v[u]) <= ethr) ? (1u << u) : 0u;
+          mk[ch >> 1] |= m << ((ch & 1) * 16);
           if (m) {
-            c1 = min(c1, c0 + __ffs(m) - 1);
+            c1 = min(c1, ch * 16 + __ffs(m) - 1);
             ncand += __popc(m);
           }
         }
@@ -415,7 +412,7 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
 
         // exact chains: every row's first candidate on its own lane, then the
         // warp's extra candidates (near-ties) spread over all 32 lanes
-        const unsigned char* xsm = f32in ? sm + lay.off_xp + b * 3 * PL_BYTES : sm + s * PL_BYTES;
+        const unsigned char* xsm = sm + s * SB;
         float best = INFINITY;
         int lbl = INT_MAX;
         if (valid && ncand >= 1) {
@@ -432,8 +429,6 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         if (total > 0) {
-          uint32_t* qe = reinterpret_cast<uint32_t*>(sm + lay.off_q) + (warp - W_EPI0) * 2 * QCAP;
-          float* qr = reinterpret_cast<float*>(qe + QCAP);
           const int off = incl - extra;
           if (total <= QCAP) {
             int e = off;
@@ -476,9 +471,8 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
           fixups += (ncand >= 2);
           wide += (ncand > 2);
         }
-        // x is no longer needed: release the planes / stage
-        if (f32in) mbar_arrive(pempty + b);
-        else mbar_arrive(xempty + s);
+        // x is no longer needed: release the stage
+        mbar_arrive(xempty + s);
 
         int label = (lbl == INT_MAX) ? c_lo : c_lo + lbl;
         if (valid) {
@@ -537,6 +531,9 @@ bool assign_tc_eligible(const ac_cluster_problem* host_probs, int nprob, int dty
     if (P.k - c_lo < 1 || P.k - c_lo > ac::asg::NBMAX) return false;
     if ((reinterpret_cast<uintptr_t>(P.x) & 15) || (reinterpret_cast<uintptr_t>(P.centers) & 15))
       return false;
+    // f32 points are read as their exact bf16 planes (written by ac_lloyd_prepare)
+    if (dtype == AC_DTYPE_F32 && (!P.planes || (reinterpret_cast<uintptr_t>(P.planes) & 15)))
+      return false;
   }
   return true;
 }
@@ -560,7 +557,9 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     int cap = 16;
     for (int j = 0; j < np; ++j)
       cap = std::max(cap, (host_probs[p0 + j].k - c_lo + 15) & ~15);
-    prm.lay = make_layout(dtype, cap);
+    int xs = 4;
+    while (xs > 1 && make_layout(dtype, cap, xs).smem > SMEM_MAX) --xs;
+    prm.lay = make_layout(dtype, cap, xs);
     if (prm.lay.smem > SMEM_MAX) {
       set_error("k_assign_tc: shared-memory layout %d B exceeds the budget", prm.lay.smem);
       return AC_ERR_PARAM;
@@ -574,13 +573,10 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
       const ac_cluster_problem& P = host_probs[p0 + j];
       const int64_t tiles = (P.n + BM - 1) / BM;
       prm.tile0[j + 1] = prm.tile0[j] + (int)tiles;
-      int rc;
-      if (dtype == AC_DTYPE_F32)
-        rc = make_map_2d(&prm.x[j], P.x, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, std::max<int64_t>(P.n, 1),
-                         DIM, 32, BM);
-      else
-        rc = make_map_2d(&prm.x[j], P.x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                         std::max<int64_t>(P.n, 1), DIM, 64, BM);
+      // bf16 points: the tile itself; f32 points: the [3][n][64] planes
+      const void* base = dtype == AC_DTYPE_F32 ? P.planes : P.x;
+      const int64_t rows = (dtype == AC_DTYPE_F32 ? 3 : 1) * std::max<int64_t>(P.n, 1);
+      int rc = make_map_2d(&prm.x[j], base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, DIM, 64, BM);
       if (rc) return rc;
     }
     const int total = prm.tile0[np];

@@ -133,6 +133,23 @@ k_problem_xx(const ac_cluster_problem* __restrict__ probs, int dtype, int d) {
   stage_rows_f32(P.x, dtype, row0, nr, d, nsm);
   __syncthreads();
   if ((int)threadIdx.x < nr) P.xx[row0 + threadIdx.x] = row_sq_pw(nsm + threadIdx.x * (d + 1), d);
+  if (P.planes && dtype == AC_DTYPE_F32) {
+    // exact split x = hi + mid + lo into bf16 planes [3][n][d] (coalesced)
+    __nv_bfloat16* pl = reinterpret_cast<__nv_bfloat16*>(P.planes);
+    const int64_t plane = P.n * d;
+    for (int e = threadIdx.x; e < nr * d; e += blockDim.x) {
+      const int r = e / d, t = e - r * d;
+      const float v = nsm[r * (d + 1) + t];
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      const float r1 = __fsub_rn(v, __bfloat162float(hi));
+      const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+      const __nv_bfloat16 lo = __float2bfloat16_rn(__fsub_rn(r1, __bfloat162float(mid)));
+      const int64_t o = row0 * d + e;
+      pl[o] = hi;
+      pl[plane + o] = mid;
+      pl[2 * plane + o] = lo;
+    }
+  }
 }
 
 __global__ void k_status_init(const ac_cluster_problem* __restrict__ probs, int nprob) {

@@ -107,6 +107,10 @@ class Batch:
         self.tile_hist = torch.empty(max(sum(t * c for t, c in zip(tiles, self.kcaps)), 1),
                                      dtype=I32, device=dev)
         self.inertia = torch.zeros(P * self.max_iter, dtype=F32, device=dev)
+        # f32 points: exact bf16 hi/mid/lo planes for the tensor-core assign
+        # (written by ac_lloyd_prepare), [3][n][D] per problem
+        self.planes = (torch.empty(3 * N * D, dtype=torch.bfloat16, device=dev)
+                       if self.dtype == L.DTYPE_F32 and D == 64 else None)
         self.status = torch.zeros(P * L.STATUS_WORDS, dtype=I32, device=dev)
         desc = np.zeros(P, dtype=L.PROBLEM_DTYPE)
         self.n_off, self.k_off, self.t_off = [], [], []
@@ -135,6 +139,7 @@ class Batch:
             e["plan_n"] = L.pw_plan(self.ns[p]).data_ptr()
             e["plan_k"] = 0
             e["dscratch"] = self.dscratch.data_ptr() + 8 * no
+            e["planes"] = (self.planes.data_ptr() + 2 * 3 * no * D) if self.planes is not None else 0
             e["n"] = self.ns[p]
             e["k"] = self.ks[p]
             e["order"] = self.orders[p]
