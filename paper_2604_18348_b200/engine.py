@@ -192,6 +192,13 @@ class Batch:
                    max(self.ns[g0:g1]), max(self.kcaps[g0:g1]), int(max_iter), float(tol),
                    int(poll_every), self.desc.ctypes.data + g0 * isz, L.stream_ptr())
 
+    def lloyd_range(self, g0: int, g1: int, max_iter: int, tol: float):
+        """Lloyd on problems [g0, g1) of the batch (current stream)."""
+        isz = self.desc.dtype.itemsize
+        L.call("ac_lloyd", self.dev.data_ptr() + g0 * isz, g1 - g0, self.dtype, self.D,
+               max(self.ns[g0:g1]), max(self.kcaps[g0:g1]), int(max_iter), float(tol), 0,
+               self.desc.ctypes.data + g0 * isz, L.stream_ptr())
+
     def l2_group(self, budget: float = 48e6) -> int:
         """Problems per block so that a block's points fit in ~`budget` bytes of L2."""
         esz = 2 if self.dtype == L.DTYPE_BF16 else 4

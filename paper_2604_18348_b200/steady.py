@@ -19,6 +19,7 @@ centres in the batch, which is exactly the next step's warm start
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -38,7 +39,7 @@ class SteadyStep:
     (valid until the next call)."""
 
     def __init__(self, H: int, Ln: int, D: int, dtype: torch.dtype, params, key_centers: list,
-                 query_centers: list, out_dtype=None, use_graph: bool = True):
+                 query_centers: list, out_dtype=None, use_graph: bool = True, split: int = 2):
         dev = L.device()
         self.H, self.L, self.D, self.dtype = H, Ln, D, dtype
         self.p = params
@@ -139,42 +140,56 @@ class SteadyStep:
         # CUDA events recorded inside the graph around the attention kernel
         # and around the clustering (kernel time of the last replay)
         self.ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
-        self.side = torch.cuda.Stream()
+        # concurrent clustering chains: head blocks x (keys, queries)
+        split = int(os.environ.get("AC_STEADY_SPLIT", split))
+        self.split = max(1, min(split, H))
+        self.hb = (H + self.split - 1) // self.split
+        nblk = (H + self.hb - 1) // self.hb
+        self.streams = [torch.cuda.Stream() for _ in range(2 * nblk)]
         self.fork = torch.cuda.Event()
-        self.join = torch.cuda.Event()
+        self.joins = [torch.cuda.Event() for _ in range(2 * nblk)]
 
     # ------------------------------------------------------------------
     def _enqueue(self):
-        """Every kernel of one warm step.  The key side (Lloyd, envelopes,
-        K/V permutation) and the query side (normalise, Lloyd, reps) are
-        independent until selection, so they run on two streams; both are
-        latency-bound chains that leave most SMs idle on their own."""
+        """Every kernel of one warm step.  Heads are independent and the key
+        side (Lloyd, envelopes, K/V permutation) and query side (normalise,
+        Lloyd, reps) only meet at selection, so the clustering runs as
+        ``2 * self.split`` concurrent chains (key / query x head blocks) on
+        separate streams: each Lloyd chain alone is a sequence of
+        latency-bound launches that leaves most SMs idle."""
         H, Ln, D = self.H, self.L, self.D
         p = self.p
         kb, qb = self.kb, self.qb
         main = torch.cuda.current_stream()
         self.ev[0].record()
-        self.fork.record(main)
-        self.side.wait_event(self.fork)
-        with torch.cuda.stream(self.side):
-            s = L.stream_ptr()
-            kb.lloyd(p.max_iter, p.tol)
-            L.call("ac_envelopes", self.env_desc.data_ptr(), H, self.dt, D, kb.max_k,
-                   self.pmax.data_ptr(), self.pmin.data_ptr(), s)
-            L.call("ac_permute_rows_heads", self.K.data_ptr(), self.dt, D, self.kperm.data_ptr(),
-                   Ln, H, self.kp.data_ptr(), s)
-            L.call("ac_permute_rows_heads", self.V.data_ptr(), self.dt, D, self.kperm.data_ptr(),
-                   Ln, H, self.vp.data_ptr(), s)
-            self.join.record(self.side)
         s = L.stream_ptr()
         L.call("ac_l2norm", self.Q.data_ptr(), self.dt, H * Ln, D, self.qn.data_ptr(), 0,
                self.qdeg.data_ptr(), s)
-        qb.lloyd(p.max_iter, p.tol)
+        self.fork.record(main)
+        blocks = [(h0, min(H, h0 + self.hb)) for h0 in range(0, H, self.hb)]
+        for i, (h0, h1) in enumerate(blocks):
+            ks, qs = self.streams[2 * i], self.streams[2 * i + 1]
+            ks.wait_event(self.fork)
+            qs.wait_event(self.fork)
+            with torch.cuda.stream(ks):
+                kb.lloyd_range(h0, h1, p.max_iter, p.tol)
+                self.joins[2 * i].record(ks)
+            with torch.cuda.stream(qs):
+                qb.lloyd_range(h0, h1, p.max_iter, p.tol)
+                self.joins[2 * i + 1].record(qs)
+        for i in range(2 * len(blocks)):
+            main.wait_event(self.joins[i])
+        s = L.stream_ptr()
         L.call("ac_segment_mean", self.reps_desc.data_ptr(), H, L.DTYPE_F32, D, self.gq,
                self.reps_ptrs.data_ptr(), s)
-        main.wait_event(self.join)
+        L.call("ac_envelopes", self.env_desc.data_ptr(), H, self.dt, D, kb.max_k,
+               self.pmax.data_ptr(), self.pmin.data_ptr(), s)
         L.call("ac_select", self.sel_desc.data_ptr(), H, D, self.scorer, self.gq, kb.max_k,
                self.stride, s)
+        L.call("ac_permute_rows_heads", self.K.data_ptr(), self.dt, D, self.kperm.data_ptr(),
+               Ln, H, self.kp.data_ptr(), s)
+        L.call("ac_permute_rows_heads", self.V.data_ptr(), self.dt, D, self.kperm.data_ptr(),
+               Ln, H, self.vp.data_ptr(), s)
         L.call("ac_build_q_layout", self.Q.data_ptr(), self.dt, D, Ln, H, self.qperm.data_ptr(),
                self.qstarts.data_ptr(), self.qcounts.data_ptr(), self.qlab.data_ptr(),
                self.gq_t.data_ptr(), self.gq, self.nruns.data_ptr(), self.stride,
