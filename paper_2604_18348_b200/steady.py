@@ -147,36 +147,54 @@ class SteadyStep:
         nblk = (H + self.hb - 1) // self.hb
         self.streams = [torch.cuda.Stream() for _ in range(2 * nblk)]
         self.fork = torch.cuda.Event()
+        self.fork_k = torch.cuda.Event()
+        self.host_graphs = {}
         self.joins = [torch.cuda.Event() for _ in range(2 * nblk)]
 
     # ------------------------------------------------------------------
-    def _enqueue(self):
+    def _enqueue(self, host=None):
         """Every kernel of one warm step.  Heads are independent and the key
         side (Lloyd, envelopes, K/V permutation) and query side (normalise,
         Lloyd, reps) only meet at selection, so the clustering runs as
         ``2 * self.split`` concurrent chains (key / query x head blocks) on
         separate streams: each Lloyd chain alone is a sequence of
-        latency-bound launches that leaves most SMs idle."""
+        latency-bound launches that leaves most SMs idle.
+
+        ``host = (hQ, hK, hV, hout)`` (pinned) puts the PCIe copies into the
+        graph: Q first (the query chain is the longest), then K, then V,
+        each overlapping the clustering already running; the result is copied
+        back at the end."""
         H, Ln, D = self.H, self.L, self.D
         p = self.p
         kb, qb = self.kb, self.qb
         main = torch.cuda.current_stream()
+        blocks = [(h0, min(H, h0 + self.hb)) for h0 in range(0, H, self.hb)]
         self.ev[0].record()
+        if host is not None:
+            self.Q.copy_(host[0], non_blocking=True)
         s = L.stream_ptr()
         L.call("ac_l2norm", self.Q.data_ptr(), self.dt, H * Ln, D, self.qn.data_ptr(), 0,
                self.qdeg.data_ptr(), s)
         self.fork.record(main)
-        blocks = [(h0, min(H, h0 + self.hb)) for h0 in range(0, H, self.hb)]
         for i, (h0, h1) in enumerate(blocks):
-            ks, qs = self.streams[2 * i], self.streams[2 * i + 1]
-            ks.wait_event(self.fork)
+            qs = self.streams[2 * i + 1]
             qs.wait_event(self.fork)
-            with torch.cuda.stream(ks):
-                kb.lloyd_range(h0, h1, p.max_iter, p.tol)
-                self.joins[2 * i].record(ks)
             with torch.cuda.stream(qs):
                 qb.lloyd_range(h0, h1, p.max_iter, p.tol)
                 self.joins[2 * i + 1].record(qs)
+        if host is not None:
+            self.K.copy_(host[1], non_blocking=True)
+            self.fork_k.record(main)
+        else:
+            self.fork_k = self.fork
+        for i, (h0, h1) in enumerate(blocks):
+            ks = self.streams[2 * i]
+            ks.wait_event(self.fork_k)
+            with torch.cuda.stream(ks):
+                kb.lloyd_range(h0, h1, p.max_iter, p.tol)
+                self.joins[2 * i].record(ks)
+        if host is not None:
+            self.V.copy_(host[2], non_blocking=True)
         for i in range(2 * len(blocks)):
             main.wait_event(self.joins[i])
         s = L.stream_ptr()
@@ -200,8 +218,10 @@ class SteadyStep:
                self.kp.data_ptr(), self.vp.data_ptr(), self.dt, D, Ln, H, self.items.data_ptr(),
                H * self.item_cap, self.runs.data_ptr(), self.scale, self.out.data_ptr(), self.odt, s)
         self.ev[2].record()
+        if host is not None:
+            host[3].copy_(self.out, non_blocking=True)
 
-    def _capture(self):
+    def _capture(self, host=None):
         # one eager run on a side stream (lazy kernel attributes, workspaces),
         # then capture; the eager run advanced the warm start, so restore it
         kc = self.kb.centers.clone()
@@ -209,16 +229,29 @@ class SteadyStep:
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            self._enqueue()
+            self._enqueue(host)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         self.kb.centers.copy_(kc)
         self.qb.centers.copy_(qc)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self._enqueue()
+            self._enqueue(host)
         torch.cuda.synchronize()
-        self.graph = g
+        return g
+
+    def step_host(self, hQ, hK, hV, hout) -> torch.Tensor:
+        """One warm step from pinned host inputs into a pinned host result
+        (copies inside the graph, overlapped with the clustering).  One graph
+        per distinct set of host buffers (a serving loop reuses a few)."""
+        key = tuple(t.data_ptr() for t in (hQ, hK, hV, hout))
+        g = self.host_graphs.get(key)
+        if g is None:
+            if len(self.host_graphs) >= 4:
+                self.host_graphs.pop(next(iter(self.host_graphs)))
+            g = self.host_graphs[key] = self._capture((hQ, hK, hV, hout))
+        g.replay()
+        return hout
 
     def step(self, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor) -> torch.Tensor:
         """One warm step; returns the static output buffer [H, L, D]."""
@@ -229,7 +262,7 @@ class SteadyStep:
             self._enqueue()
         else:
             if self.graph is None:
-                self._capture()
+                self.graph = self._capture()
             self.graph.replay()
         return self.out
 
