@@ -48,6 +48,12 @@ constexpr int NBAR = 1 + 2 * STAGES + 2 + 2 + 2 + 2;
 constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
 constexpr int SMEM = OFF_MISC + 16 + 1024;
 constexpr uint32_t COL_S = 0, COL_O = 256, COL_P = 384;
+#ifndef AC_FA4_ORDER
+#define AC_FA4_ORDER 1  // MMA issue order per K tile (0: S0 S1 PV0 PV1, 1: S0 PV0 S1 PV1)
+#endif
+#ifndef AC_FA4_POLY
+#define AC_FA4_POLY 0  // of every 8 exp2 pairs, this many on the FMA pipe (polynomial)
+#endif
 
 AC_DEV void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                     uint32_t accum) {
@@ -239,12 +245,21 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
         fence_after();
         // S for tile j as soon as each softmax has pulled S_{j-1} into
         // registers, then the PV products of tile j-1 once P_{j-1} is in TMEM
+#if AC_FA4_ORDER == 0
         issue_s(0, j, st);
         if (two) issue_s(1, j, st);
         if (j > 0) {
           issue_pv(0, j - 1, (j - 1) % STAGES);
           if (two) issue_pv(1, j - 1, (j - 1) % STAGES);
         }
+#else
+        issue_s(0, j, st);
+        if (j > 0) issue_pv(0, j - 1, (j - 1) % STAGES);
+        if (two) {
+          issue_s(1, j, st);
+          if (j > 0) issue_pv(1, j - 1, (j - 1) % STAGES);
+        }
+#endif
         if (j > 0) umma_commit(kv_empty + (j - 1) % STAGES);
         ++j;
       }
@@ -319,7 +334,7 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
                 fma2(pk2(__uint_as_float(sr[ch][2 * i]), __uint_as_float(sr[ch][2 * i + 1])), sc, nm);
             float x0, x1, p0, p1;
             up2(x, x0, x1);
-            if ((i & 7) < 3) {
+            if ((i & 7) < AC_FA4_POLY) {
               exp2_poly2(x0, x1, p0, p1);
             } else {
               p0 = ex2(x0);
