@@ -419,7 +419,7 @@ def main():
                                            "per-head seed 1000+h)",
             "config": config_block(cfg, world),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "frac": achieved / peak if peak else None, "traffic": attn_traffic(),
                          "kernel": "ac_sparse_attention", "peak_kind": f"{pk_kind} sustained bf16",
                          "useful_flops_per_step": useful, "kernel_ms_per_step": attn_ms},
             "cpu_baseline": cpu,
@@ -438,14 +438,14 @@ def main():
         dist.destroy_process_group()
 
 
-def attention_flops(last, D):
-    """Useful attention FLOPs of one step: 4·D·Σ_heads Σ_g |Q_g|·|S_g|."""
-    import torch
-    qm, km, so = last
-    tot = torch.zeros((), dtype=torch.float64, device="cuda")
-    for h, sel in enumerate(so.selections):
-        tot += (qm[h].counts.double() * sel._covered.double()).sum()
-    return tot * 4.0 * D
+def attn_traffic():
+    """DRAM bytes (read + write) per launch of the attention kernel from the
+    committed ncu --set full capture (profiles/r01_traffic.json), or None."""
+    try:
+        t = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())
+        return t["k_attn_fa4"]["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def count_launches(sess, dev_in, gather, args) -> int:
@@ -482,19 +482,35 @@ def dense_sdpa_ms(trip, tdt):
 
 
 def cpu_baseline(sess, host, args, cfg):
-    """Oracle port of head 0's next warm step, started from the GPU session's
-    carried (bit-identical) state."""
+    """Head 0's next warm step on the host cores, started from the GPU
+    session's carried state (bit-identical to the reference's own): the
+    unmodified reference package (baseline/_ref) when installed, else the
+    bit-exact oracle port."""
     import torch
     idx = (args.warmup + args.steps + 1) % 2
     q, k, v = (host[idx][j][0].float().numpy() for j in range(3))
     kc = sess.key_centers[0].cpu().numpy()
     qc = sess.query_centers[0].cpu().numpy()
-    dt, r, _ = cpu_warm_step(q, k, v, kc, qc)
+    R = _reference_pkg()
+    if R is not None:
+        from threadpoolctl import threadpool_limits
+        cores = os.cpu_count() or 1
+        with threadpool_limits(cores):
+            p = R.PipelineParams(q_clusters=65, topk=25, m0=100, n_max=1000, full_layer_quota=0.0)
+            pol = R.LayerPolicy(mode="sparse", topk=25)
+            st = R.StepState(step=1, key_centers=kc, query_centers=qc)
+            t0 = time.perf_counter()
+            R.adacluster_attention(q, k, v, pol, st, 0, p)
+            dt = time.perf_counter() - t0
+        kind, what = "reference", "adacluster (baseline/_ref) with all host threads"
+    else:
+        dt, _, _ = cpu_warm_step(q, k, v, kc, qc)
+        cores, kind = cpu_threads(), "port"
+        what = "oracle port: clustering in C threads, attention in numpy/OpenBLAS"
     layer = dt * cfg["heads"]
-    return {"value": cfg["seq"] / layer, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
+    return {"value": cfg["seq"] / layer, "unit": "tokens/s", "cores": cores, "kind": kind,
             "sample": f"head 0 of {cfg['heads']}, one warm step at L={cfg['seq']} "
-                      f"({dt:.1f}s), x{cfg['heads']} extrapolated; clustering in C threads, "
-                      "attention in numpy/OpenBLAS"}
+                      f"({dt:.1f}s), x{cfg['heads']} extrapolated; {what}"}
 
 
 if __name__ == "__main__":

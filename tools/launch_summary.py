@@ -5,7 +5,7 @@ h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[h]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
 agg = collections.defaultdict(lambda: [0, 0.0])
-scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+scale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3}
 for r in rows[h + 1:]:
     if len(r) <= vi:
         continue
