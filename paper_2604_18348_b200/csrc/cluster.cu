@@ -754,45 +754,56 @@ k_update_w(const ac_cluster_problem* __restrict__ probs, int d, double tol, int 
     __syncwarp();
     const unsigned char* cur = ring + (size_t)(b % kUpdWStages) * stage_bytes + lane * DPL * ESZ;
     const int rows = min(kUpdWRows, cnt - b * kUpdWRows);
-    float v[kUpdWRows][DPL];
+    // 8 rows at a time: loads of the next group overlap the f64 chain of this one
+    auto load8 = [&](int r0, float (&v)[8][DPL]) {
 #pragma unroll
-    for (int r = 0; r < kUpdWRows; ++r) {
-      const unsigned char* rp = cur + r * row_bytes;
-      if constexpr (BF16) {
-        if constexpr (DPL == 2) {
-          const uint32_t w = *reinterpret_cast<const uint32_t*>(rp);
-          v[r][0] = __uint_as_float(w << 16); v[r][1] = __uint_as_float(w & 0xffff0000u);
+      for (int r = 0; r < 8; ++r) {
+        const unsigned char* rp = cur + (r0 + r) * row_bytes;
+        if constexpr (BF16) {
+          if constexpr (DPL == 2) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(rp);
+            v[r][0] = __uint_as_float(w << 16); v[r][1] = __uint_as_float(w & 0xffff0000u);
+          } else {
+            const uint2 w = *reinterpret_cast<const uint2*>(rp);
+            v[r][0] = __uint_as_float(w.x << 16); v[r][1] = __uint_as_float(w.x & 0xffff0000u);
+            v[r][2] = __uint_as_float(w.y << 16); v[r][3] = __uint_as_float(w.y & 0xffff0000u);
+          }
         } else {
-          const uint2 w = *reinterpret_cast<const uint2*>(rp);
-          v[r][0] = __uint_as_float(w.x << 16); v[r][1] = __uint_as_float(w.x & 0xffff0000u);
-          v[r][2] = __uint_as_float(w.y << 16); v[r][3] = __uint_as_float(w.y & 0xffff0000u);
-        }
-      } else {
-        if constexpr (DPL == 2) {
-          const float2 f = *reinterpret_cast<const float2*>(rp);
-          v[r][0] = f.x; v[r][1] = f.y;
-        } else {
-          const float4 f = *reinterpret_cast<const float4*>(rp);
-          v[r][0] = f.x; v[r][1] = f.y; v[r][2] = f.z; v[r][3] = f.w;
+          if constexpr (DPL == 2) {
+            const float2 f = *reinterpret_cast<const float2*>(rp);
+            v[r][0] = f.x; v[r][1] = f.y;
+          } else {
+            const float4 f = *reinterpret_cast<const float4*>(rp);
+            v[r][0] = f.x; v[r][1] = f.y; v[r][2] = f.z; v[r][3] = f.w;
+          }
         }
       }
-    }
-    if (b == 0) {
+    };
+    if (rows == kUpdWRows && b > 0) {  // full stage: no per-row guards
 #pragma unroll
-      for (int i = 0; i < DPL; ++i) acc[i] = (double)v[0][i];  // first member initialises
-    }
-    if (rows == kUpdWRows && b > 0) {
+      for (int r0 = 0; r0 < kUpdWRows; r0 += 8) {
+        float v[8][DPL];
+        load8(r0, v);
 #pragma unroll
-      for (int r = 0; r < kUpdWRows; ++r)
+        for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int i = 0; i < DPL; ++i) acc[i] = __dadd_rn(acc[i], (double)v[r][i]);
+          for (int i = 0; i < DPL; ++i) acc[i] = __dadd_rn(acc[i], (double)v[r][i]);
+      }
     } else {
+      for (int r0 = 0; r0 < rows; r0 += 8) {
+        float v[8][DPL];
+        load8(r0, v);  // (rows past `rows` read stale ring bytes and are skipped)
 #pragma unroll
-      for (int r = 0; r < kUpdWRows; ++r) {
-        if (r >= rows) break;
-        if (b == 0 && r == 0) continue;
+        for (int r = 0; r < 8; ++r) {
+          if (r0 + r >= rows) break;
+          if (b == 0 && r0 + r == 0) {
 #pragma unroll
-        for (int i = 0; i < DPL; ++i) acc[i] = __dadd_rn(acc[i], (double)v[r][i]);
+            for (int i = 0; i < DPL; ++i) acc[i] = (double)v[r][i];  // first member initialises
+            continue;
+          }
+#pragma unroll
+          for (int i = 0; i < DPL; ++i) acc[i] = __dadd_rn(acc[i], (double)v[r][i]);
+        }
       }
     }
     __syncwarp();  // the stage is refilled by the next issue
