@@ -154,6 +154,14 @@ int ac_lloyd(const ac_cluster_problem* probs, int nprob, int dtype, int d,
              int64_t max_n, int max_k, int max_iter, double tol,
              int poll_every, const ac_cluster_problem* host_probs, void* stream);
 
+/* ac_lloyd with flags (no host polling): AC_LLOYD_NO_INERTIA skips the
+ * per-iteration inertia_history reduction (steady-state steps never read it;
+ * labels, centres and n_iter are unaffected).                               */
+#define AC_LLOYD_NO_INERTIA 1
+int ac_lloyd_ex(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                int64_t max_n, int max_k, int max_iter, double tol, int flags,
+                const ac_cluster_problem* host_probs, void* stream);
+
 /* Single passes, exposed for the multi-stage planner and for tests. */
 int ac_lloyd_prepare(const ac_cluster_problem* probs, int nprob, int dtype,
                      int d, int64_t max_n, int max_k, void* stream);

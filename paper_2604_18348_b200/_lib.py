@@ -25,6 +25,7 @@ SCORERS = {"quest": 0, "mean": 1, "clamped": 2, "given": 3}
 ASSIGN_MERGE, ASSIGN_ALL = 1, 2
 ST_ACTIVE, ST_NITER, ST_DONE, ST_FLAGS, ST_KPP_STOP, ST_REPAIRS, ST_FIXUPS, ST_WIDE = range(8)
 ASSIGN_MODE_AUTO, ASSIGN_MODE_EXACT, ASSIGN_MODE_TC = range(3)
+LLOYD_NO_INERTIA = 1
 STATUS_WORDS = 8
 
 # struct layouts (must match the header; checked in tests/test_abi.py)
@@ -63,6 +64,7 @@ _SIGS = {
     "ac_row_sqnorm": [_P, _I, _I64, _I, _P, _P],
     "ac_kmeanspp": [_P, _I, _I, _I, _I64, _I, _P, _P],
     "ac_lloyd": [_P, _I, _I, _I, _I64, _I, _I, _D, _I, _P, _P],
+    "ac_lloyd_ex": [_P, _I, _I, _I, _I64, _I, _I, _D, _I, _P, _P],
     "ac_lloyd_prepare": [_P, _I, _I, _I, _I64, _I, _P],
     "ac_assign": [_P, _I, _I, _I, _I64, _I, _I, _I, _P],
     "ac_assign_ordered": [_P, _I, _I, _I, _I64, _I, _I, _I, _I, _P, _P],

@@ -1207,9 +1207,15 @@ extern "C" int ac_lloyd_prepare(const ac_cluster_problem* probs, int nprob, int 
 
 // `generic` is decided per batch by the host (every problem of a batch shares
 // one accumulation order; the host splits batches otherwise).
+// internal assign flag: ||c||^2 is already current (inside a Lloyd run the
+// centroid update writes it), skip k_center_sqnorm
+constexpr int kAssignCcValid = 1 << 8;
+
 static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
                        int64_t max_n, int max_k, int c_lo, int flags, int order,
                        const ac_cluster_problem* host_probs, cudaStream_t st) {
+  const bool cc_valid = flags & kAssignCcValid;
+  flags &= ~kAssignCcValid;
   const unsigned tiles = (unsigned)((max_n + kAsgBM - 1) / kAsgBM);
   const int mode = g_assign_mode;
   const bool tc_ok = ac_host::assign_tc_eligible(host_probs, nprob, dtype, d, c_lo, order);
@@ -1219,7 +1225,7 @@ static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
     return AC_ERR_PARAM;
   }
   if (tc_ok && mode != AC_ASSIGN_MODE_EXACT) {
-    k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
+    if (!cc_valid) k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
     AC_CHECK_LAUNCH("k_center_sqnorm");
     return ac_host::assign_tc_launch(probs, host_probs, nprob, dtype, c_lo, flags, st);
   }
@@ -1227,13 +1233,13 @@ static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
     const size_t smem = assign_smem_bytes(d, max_k);
     int rc = set_smem((const void*)k_assign_seq, smem);
     if (rc) return rc;
-    k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
+    if (!cc_valid) k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
     k_assign_seq<<<dim3(tiles, nprob), 256, smem, st>>>(probs, dtype, d, c_lo, flags, max_k);
   } else {
     const size_t smem = sizeof(int) * (size_t)(max_k + 4);
     int rc = set_smem((const void*)k_assign_generic, smem);
     if (rc) return rc;
-    k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
+    if (!cc_valid) k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
     k_assign_generic<<<dim3(tiles, nprob), kAsgBM, smem, st>>>(probs, dtype, d, c_lo, flags, max_k);
   }
   AC_CHECK_LAUNCH("ac_assign");
@@ -1319,9 +1325,9 @@ extern "C" int ac_segment_mean(const ac_cluster_problem* probs, int nprob, int d
   return update_impl(probs, nprob, dtype, d, max_k, 0.0, 1, out, S(stream));
 }
 
-extern "C" int ac_lloyd(const ac_cluster_problem* probs, int nprob, int dtype, int d,
-                        int64_t max_n, int max_k, int max_iter, double tol, int poll_every,
-                        const ac_cluster_problem* host_probs, void* stream) {
+static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                      int64_t max_n, int max_k, int max_iter, double tol, int poll_every,
+                      int lflags, const ac_cluster_problem* host_probs, void* stream) {
   if (nprob <= 0) return AC_OK;
   if (d < 1 || d > 256) { ac_host::set_error("lloyd: d=%d unsupported (1..256)", d); return AC_ERR_DIM; }
   if (max_k > 16384) { ac_host::set_error("lloyd: k=%d too large", max_k); return AC_ERR_PARAM; }
@@ -1329,13 +1335,17 @@ extern "C" int ac_lloyd(const ac_cluster_problem* probs, int nprob, int dtype, i
   // every problem of a batch must share the accumulation order
   int order = AC_ORDER_SEQ;
   if (host_probs) order = host_probs[0].order;
+  const bool inertia = !(lflags & AC_LLOYD_NO_INERTIA);
   int rc = ac_lloyd_prepare(probs, nprob, dtype, d, max_n, max_k, stream);
   if (rc) return rc;
   int32_t* pinned = nullptr;
   if (poll_every > 0 && host_probs) cudaMallocHost(&pinned, sizeof(int32_t) * nprob);
   for (int it = 0; it < max_iter; ++it) {
-    if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, 0, order, host_probs, st))) break;
-    if ((rc = repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, it, 0, st))) break;
+    // ||c||^2 is current: prepare wrote it, then every centroid update does
+    if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, kAssignCcValid, order,
+                          host_probs, st)))
+      break;
+    if ((rc = repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, inertia ? it : -1, 0, st))) break;
     if ((rc = update_impl(probs, nprob, dtype, d, max_k, tol, 0, nullptr, st))) break;
     if (pinned && (it + 1) % poll_every == 0 && it + 1 < max_iter) {
       for (int p = 0; p < nprob; ++p)
@@ -1349,10 +1359,24 @@ extern "C" int ac_lloyd(const ac_cluster_problem* probs, int nprob, int dtype, i
   }
   if (pinned) cudaFreeHost(pinned);
   if (rc) return rc;
-  if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, AC_ASSIGN_ALL, order, host_probs,
-                        st)))
+  if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, AC_ASSIGN_ALL | kAssignCcValid,
+                        order, host_probs, st)))
     return rc;
   return repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, -1, AC_ASSIGN_ALL, st);
+}
+
+extern "C" int ac_lloyd(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                        int64_t max_n, int max_k, int max_iter, double tol, int poll_every,
+                        const ac_cluster_problem* host_probs, void* stream) {
+  return lloyd_impl(probs, nprob, dtype, d, max_n, max_k, max_iter, tol, poll_every, 0, host_probs,
+                    stream);
+}
+
+extern "C" int ac_lloyd_ex(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                           int64_t max_n, int max_k, int max_iter, double tol, int flags,
+                           const ac_cluster_problem* host_probs, void* stream) {
+  return lloyd_impl(probs, nprob, dtype, d, max_n, max_k, max_iter, tol, 0, flags, host_probs,
+                    stream);
 }
 
 extern "C" int ac_kmeanspp(const ac_cluster_problem* probs, int nprob, int dtype, int d,

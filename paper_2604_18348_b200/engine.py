@@ -192,12 +192,14 @@ class Batch:
                    max(self.ns[g0:g1]), max(self.kcaps[g0:g1]), int(max_iter), float(tol),
                    int(poll_every), self.desc.ctypes.data + g0 * isz, L.stream_ptr())
 
-    def lloyd_range(self, g0: int, g1: int, max_iter: int, tol: float):
-        """Lloyd on problems [g0, g1) of the batch (current stream)."""
+    def lloyd_range(self, g0: int, g1: int, max_iter: int, tol: float, inertia: bool = True):
+        """Lloyd on problems [g0, g1) of the batch (current stream);
+        ``inertia=False`` skips the inertia_history reductions."""
         isz = self.desc.dtype.itemsize
-        L.call("ac_lloyd", self.dev.data_ptr() + g0 * isz, g1 - g0, self.dtype, self.D,
-               max(self.ns[g0:g1]), max(self.kcaps[g0:g1]), int(max_iter), float(tol), 0,
-               self.desc.ctypes.data + g0 * isz, L.stream_ptr())
+        L.call("ac_lloyd_ex", self.dev.data_ptr() + g0 * isz, g1 - g0, self.dtype, self.D,
+               max(self.ns[g0:g1]), max(self.kcaps[g0:g1]), int(max_iter), float(tol),
+               0 if inertia else L.LLOYD_NO_INERTIA, self.desc.ctypes.data + g0 * isz,
+               L.stream_ptr())
 
     def l2_group(self, budget: float = 48e6) -> int:
         """Problems per block so that a block's points fit in ~`budget` bytes of L2."""

@@ -180,7 +180,7 @@ class SteadyStep:
             qs = self.streams[2 * i + 1]
             qs.wait_event(self.fork)
             with torch.cuda.stream(qs):
-                qb.lloyd_range(h0, h1, p.max_iter, p.tol)
+                qb.lloyd_range(h0, h1, p.max_iter, p.tol, inertia=False)
                 self.joins[2 * i + 1].record(qs)
         if host is not None:
             self.K.copy_(host[1], non_blocking=True)
@@ -191,7 +191,7 @@ class SteadyStep:
             ks = self.streams[2 * i]
             ks.wait_event(self.fork_k)
             with torch.cuda.stream(ks):
-                kb.lloyd_range(h0, h1, p.max_iter, p.tol)
+                kb.lloyd_range(h0, h1, p.max_iter, p.tol, inertia=False)
                 self.joins[2 * i].record(ks)
         if host is not None:
             self.V.copy_(host[2], non_blocking=True)
