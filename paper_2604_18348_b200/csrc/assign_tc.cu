@@ -363,6 +363,13 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       float* qr = reinterpret_cast<float*>(qe + QCAP);
       const int nch = nbp >> 4;  // 16-column chunks
       int fixups = 0, wide = 0;
+      // ||x||^2 of this warpgroup's next tile, prefetched one tile ahead
+      auto load_xx = [&](int i) -> float {
+        const int64_t rw = (int64_t)(t + i - ptile0) * BM + r;
+        return (i < T && rw < n) ? P.xx[rw] : 0.f;
+      };
+      const int i_first = ((g0 & 1) == wg) ? 0 : 1;
+      float xx_next = load_xx(i_first);
       for (int i = 0; i < T; ++i) {
         const int g = g0 + i;
         if ((g & 1) != wg) continue;
@@ -370,7 +377,8 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const int tile = t + i - ptile0;
         const int64_t row = (int64_t)tile * BM + r;
         const bool valid = row < n;
-        const float xx = valid ? P.xx[row] : 0.f;
+        const float xx = xx_next;
+        xx_next = load_xx(i + 2);
         const float tb = 0x1p-15f * sqrtf(xx) * cmax + 0x1p-17f * (xx + ccmax) + 1e-30f;
         mbar_wait_sleep(afull + b, (g >> 1) & 1, 26);
         fence_after();
