@@ -48,6 +48,17 @@ AC_DEV void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
   }
 }
 
+// non-blocking phase test
+AC_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // try_wait with a suspend-time hint: the waiting thread sleeps until the
 // phase completes (or the hint expires) instead of spinning on the issue
 // slots that the working warps of the same SM sub-partition need
