@@ -1,6 +1,6 @@
 # rebuild the attention unit with variant macros and time the step
 rm -f gpurun_out/sweep.txt; mkdir -p gpurun_out
-for cfg in "-DAC_FA4_ORDER=1" "-DAC_FA4_ORDER=2"; do
+for cfg in "-DAC_FA4_SKIP=0" "-DAC_FA4_SKIP=1"; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --extended-lambda --expt-relaxed-constexpr -Iinclude $cfg -c paper_2604_18348_b200/csrc/attn_fa4.cu -o build/csrc/attn_fa4.cu.o
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_2604_18348_b200/libadacluster_sm100.so build/csrc/*.o -lcudart
   echo "$cfg" >> gpurun_out/sweep.txt
