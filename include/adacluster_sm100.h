@@ -91,6 +91,10 @@ typedef struct ac_cluster_problem {
   void* planes;         /* optional, f32 points only: [3][n][d] bf16 hi/mid/lo
                            split of x (written by ac_lloyd_prepare); enables
                            the tensor-core assignment for f32 points           */
+  double* csum;         /* optional [kcap, d] f64 (zeros),                     */
+  float* cabs;          /* [kcap, d] f32 (zeros) and                           */
+  int32_t* clsb;        /* [kcap, d] f32 bits (+inf = 0x7f800000): workspaces of the
+                           split-chain centroid update for d = 64/128          */
   int64_t n;
   int32_t k;
   int32_t order;        /* AC_ORDER_* of the reference's x @ centres.T        */
@@ -186,6 +190,12 @@ int ac_assign_ordered(const ac_cluster_problem* probs, int nprob, int dtype,
 #define AC_ASSIGN_MODE_TC 2
 int ac_set_assign_mode(int mode);
 int ac_get_assign_mode(void);
+/* centroid-update kernel selection (process-wide): 0 = split-chain sums with
+ * an exact f32 enclosure test (member-order chain per dimension only when
+ * the enclosure straddles a rounding boundary) when the batch has csum/cabs
+ * workspaces, 1 = always the member-order f64 chains.  Both are
+ * bit-identical to np.add.reduceat in member order.                        */
+int ac_set_update_mode(int mode);
 int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dtype,
                    int d, int64_t max_n, int max_k, int iter, int flags,
                    void* stream);

@@ -33,7 +33,8 @@ PROBLEM_DTYPE = np.dtype([
     ("x", "u8"), ("xx", "u8"), ("centers", "u8"), ("cc", "u8"), ("labels", "u8"),
     ("best", "u8"), ("counts", "u8"), ("perm", "u8"), ("starts", "u8"), ("tile_hist", "u8"),
     ("inertia", "u8"), ("movement", "u8"), ("status", "u8"), ("plan_n", "u8"),
-    ("plan_k", "u8"), ("dscratch", "u8"), ("planes", "u8"), ("n", "i8"), ("k", "i4"),
+    ("plan_k", "u8"), ("dscratch", "u8"), ("planes", "u8"),
+    ("csum", "u8"), ("cabs", "u8"), ("clsb", "u8"), ("n", "i8"), ("k", "i4"),
     ("order", "i4"),
 ])
 SELECT_DTYPE = np.dtype([
@@ -70,6 +71,7 @@ _SIGS = {
     "ac_assign_ordered": [_P, _I, _I, _I, _I64, _I, _I, _I, _I, _P, _P],
     "ac_set_assign_mode": [_I],
     "ac_get_assign_mode": [],
+    "ac_set_update_mode": [_I],
     "ac_repair_sort": [_P, _I, _I, _I, _I64, _I, _I, _I, _P],
     "ac_segment_mean": [_P, _I, _I, _I, _I, _P, _P],
     "ac_sort_by_label": [_P, _I, _I64, _I, _P],

@@ -843,6 +843,224 @@ k_update_w(const ac_cluster_problem* __restrict__ probs, int d, double tol, int 
 }
 
 // ---------------------------------------------------------------------------
+// K4, split-chain form (d = 64/128).  The reference sums each cluster's
+// members in f64, in member order (np.add.reduceat), divides by the count
+// and rounds to f32.  Any summation order of n values has error
+// <= (n-1)·u·Σ|x| (u = 2^-53), so the reference's f64 sum s_ref and a sum Σ
+// formed in ANY order satisfy |s_ref - Σ| <= 2n·u·Σ|x|; f32(fl64(s/n)) is
+// monotone in s, so when both ends of that enclosure round to the same f32
+// value it IS the reference's value, bit for bit.
+//
+//   k_usum   one warp per 128-member chunk of the member order (chunks may
+//            straddle clusters): f64 Σx and f32 Σ|x| per (cluster, dim) in
+//            registers, flushed with global reductions at cluster ends —
+//            the long per-cluster chains are split over many warps;
+//   k_ufin   one warp per centre: the enclosure test per dimension (and
+//            re-zeroing of the workspaces); the rare dimension whose
+//            enclosure straddles an f32 rounding boundary is recomputed with
+//            the reference's own sequential chain; then movement / ||c||^2 /
+//            convergence exactly as k_update.
+// ---------------------------------------------------------------------------
+constexpr int kUsChunk = 128;  // members per warp task
+constexpr int kUsWarps = 8;
+
+// lane's DPL consecutive dimensions of row `row` (one vector load)
+template <int DPL, bool BF16>
+AC_DEV void load_row_part(const void* x, int64_t row, int d, int lane, float (&v)[DPL]) {
+  if constexpr (BF16) {
+    const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(x) + row * d + lane * DPL;
+    if constexpr (DPL == 2) {
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
+      v[0] = __uint_as_float(w << 16); v[1] = __uint_as_float(w & 0xffff0000u);
+    } else {
+      const uint2 w = *reinterpret_cast<const uint2*>(p);
+      v[0] = __uint_as_float(w.x << 16); v[1] = __uint_as_float(w.x & 0xffff0000u);
+      v[2] = __uint_as_float(w.y << 16); v[3] = __uint_as_float(w.y & 0xffff0000u);
+    }
+  } else {
+    const float* p = reinterpret_cast<const float*>(x) + row * d + lane * DPL;
+    if constexpr (DPL == 2) {
+      const float2 f = *reinterpret_cast<const float2*>(p);
+      v[0] = f.x; v[1] = f.y;
+    } else {
+      const float4 f = *reinterpret_cast<const float4*>(p);
+      v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+    }
+  }
+}
+
+template <int DPL, bool BF16>
+__global__ void __launch_bounds__(32 * kUsWarps)
+k_usum(const ac_cluster_problem* __restrict__ probs, int d) {
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  if (P.status[AC_ST_ACTIVE] == 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = ((int64_t)blockIdx.x * kUsWarps + warp) * kUsChunk;
+  const int64_t n = P.n;
+  if (m0 >= n) return;
+  const int m1 = (int)min((int64_t)kUsChunk, n - m0);  // members in this chunk
+  const int k = P.k;
+  // cluster of member m0: the last c with starts[c] <= m0
+  int lo = 0, hi = k - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.starts[mid] <= m0) lo = mid; else hi = mid - 1;
+  }
+  int c = lo;
+  int64_t c_end = P.starts[c + 1];
+  double acc[DPL];
+  float ab[DPL];
+  float amin[DPL];  // smallest |x| (its exponent bounds every member's last bit)
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) { acc[i] = 0.0; ab[i] = 0.f; amin[i] = INFINITY; }
+  auto flush = [&]() {
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      const int64_t e = (int64_t)c * d + lane * DPL + i;
+      atomicAdd(P.csum + e, acc[i]);
+      atomicAdd(P.cabs + e, ab[i]);
+      atomicMin(P.clsb + e, __float_as_int(amin[i]));  // >= 0: int order == float order
+      acc[i] = 0.0;
+      ab[i] = 0.f;
+      amin[i] = INFINITY;
+    }
+  };
+  int pj_next = (lane < m1) ? P.perm[m0 + lane] : 0;
+  for (int j = 0; j < m1; j += 32) {
+    const int pj = pj_next;  // member indices of this 32-member group (prefetched)
+    pj_next = (j + 32 + lane < m1) ? P.perm[m0 + j + 32 + lane] : 0;
+    for (int g = 0; g < 32; g += 8) {
+      if (j + g >= m1) break;
+      float v[8][DPL];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int row = __shfl_sync(0xffffffffu, pj, g + r);
+        if (j + g + r < m1) load_row_part<DPL, BF16>(P.x, row, d, lane, v[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int64_t m = m0 + j + g + r;
+        if (j + g + r >= m1) break;
+        while (m >= c_end) {  // cluster boundary (warp-uniform)
+          flush();
+          ++c;
+          c_end = P.starts[c + 1];
+        }
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          acc[i] = __dadd_rn(acc[i], (double)v[r][i]);
+          ab[i] = __fadd_rn(ab[i], fabsf(v[r][i]));
+          amin[i] = fminf(amin[i], fabsf(v[r][i]));
+        }
+      }
+    }
+  }
+  flush();
+}
+
+template <int DPL, bool BF16>
+__global__ void __launch_bounds__(128)
+k_ufin(const ac_cluster_problem* __restrict__ probs, int d, double tol) {
+  __shared__ float s_sq[4][2][256];
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  if (P.status[AC_ST_ACTIVE] == 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 4 + warp;
+  const int k = P.k;
+  if (c >= k) return;
+  const int cnt = P.counts[c], s0 = P.starts[c];
+  const double dn = (double)cnt;
+  float nvs[DPL];
+  uint32_t fail = 0;
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    const int64_t e = (int64_t)c * d + lane * DPL + i;
+    const double sum = P.csum[e];
+    const double sab = (double)P.cabs[e] * (1.0 + dn * 0x1p-23);
+    const float amin = __int_as_float(P.clsb[e]);
+    P.csum[e] = 0.0;
+    P.cabs[e] = 0.f;
+    P.clsb[e] = 0x7f800000;  // +inf
+    // (a) every member is a multiple of 2^q (q = exponent of the smallest
+    //     |x| minus 23: an f32 has 24 significant bits) and Σ|x| < 2^(53+q):
+    //     no partial sum of ANY order rounds, so Σ is exactly the
+    //     reference's sum;
+    // (b) otherwise the order-free enclosure must land on one f32 value
+    if (amin > 0.f && sab < ldexp(1.0, 53 + ilogbf(amin) - 23)) {
+      nvs[i] = __double2float_rn(__ddiv_rn(sum, dn));
+    } else {
+      const double err = 2.02 * dn * 0x1p-53 * sab + 1e-300;
+      const float lo = __double2float_rn(__ddiv_rn(__dsub_rd(sum, err), dn));
+      const float hi = __double2float_rn(__ddiv_rn(__dadd_ru(sum, err), dn));
+      nvs[i] = lo;
+      if (!(lo == hi)) fail |= 1u << i;
+    }
+  }
+  // rare: the enclosure straddles an f32 rounding boundary -> the reference's
+  // own sequential f64 chain over the members (first member initialises)
+  unsigned lanes = __ballot_sync(0xffffffffu, fail != 0);
+  while (lanes) {
+    const int src = __ffs(lanes) - 1;
+    lanes &= lanes - 1;
+    const uint32_t f = __shfl_sync(0xffffffffu, fail, src);
+    for (int i = 0; i < DPL; ++i) {
+      if (!(f & (1u << i))) continue;
+      const int t = src * DPL + i;
+      // 128 members per round in flight, then the ordered chain
+      double acc = 0.0;
+      for (int base = 0; base < cnt; base += 128) {
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int m = base + 32 * q + lane;
+          v[q] = (m < cnt) ? ld_elem(P.x, BF16 ? AC_DTYPE_BF16 : AC_DTYPE_F32,
+                                     (int64_t)P.perm[s0 + m] * d + t)
+                           : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int nr = min(32, cnt - base - 32 * q);
+          for (int r = 0; r < nr; ++r) {
+            const double vv = (double)__shfl_sync(0xffffffffu, v[q], r);
+            acc = (base == 0 && q == 0 && r == 0) ? vv : __dadd_rn(acc, vv);
+          }
+        }
+      }
+      const float nv = __double2float_rn(__ddiv_rn(acc, dn));
+      if (lane == src) nvs[i] = nv;
+    }
+  }
+  float* dst = P.centers + (int64_t)c * d;
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    const int t = lane * DPL + i;
+    const float nv = nvs[i];
+    const float df = __fsub_rn(nv, dst[t]);
+    s_sq[warp][0][t] = __fmul_rn(df, df);
+    s_sq[warp][1][t] = __fmul_rn(nv, nv);
+    dst[t] = nv;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const float* a = s_sq[warp][0];
+    const float* bq = s_sq[warp][1];
+    P.movement[c] = __fsqrt_rn(pw_sum<float>([&](int i) { return a[i]; }, d));
+    P.cc[c] = pw_sum<float>([&](int i) { return bq[i]; }, d);
+    __threadfence();
+    const int prev = atomicAdd(&P.status[AC_ST_DONE], 1);
+    if (prev == k - 1) {
+      __threadfence();
+      const volatile float* mv = P.movement;
+      const float sm = pw_sum<float>([&](int i) { return mv[i]; }, k);
+      const float mean = __double2float_rn(__ddiv_rn((double)sm, (double)k));
+      P.status[AC_ST_DONE] = 0;
+      P.status[AC_ST_NITER] += 1;
+      if ((double)mean < tol) P.status[AC_ST_ACTIVE] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2: k-means++ seeding (clustering.py:78-91)
 // ---------------------------------------------------------------------------
 __global__ void k_kpp_init(const ac_cluster_problem* __restrict__ probs, int dtype, int d,
@@ -1148,6 +1366,7 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
 
 namespace {
 int g_assign_mode = AC_ASSIGN_MODE_AUTO;
+int g_update_mode = 0;  // 0: split-chain update when eligible, 1: member-order chains
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int set_smem(const void* fn, size_t bytes) {
@@ -1270,6 +1489,14 @@ extern "C" int ac_set_assign_mode(int mode) {
   return AC_OK;
 }
 extern "C" int ac_get_assign_mode(void) { return g_assign_mode; }
+extern "C" int ac_set_update_mode(int mode) {
+  if (mode < 0 || mode > 1) {
+    ac_host::set_error("ac_set_update_mode: bad mode %d", mode);
+    return AC_ERR_PARAM;
+  }
+  g_update_mode = mode;
+  return AC_OK;
+}
 
 static int repair_sort_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
                             int64_t max_n, int max_k, int iter, int flags, cudaStream_t st) {
@@ -1288,6 +1515,34 @@ extern "C" int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dt
                               int64_t max_n, int max_k, int iter, int flags, void* stream) {
   if (nprob <= 0 || max_n <= 0) return AC_OK;
   return repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, iter, flags, S(stream));
+}
+
+// split-chain update (k_usum + k_ufin) for a Lloyd iteration
+static int usum_update_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                            int64_t max_n, int max_k, double tol, cudaStream_t st) {
+  const bool bf = dtype == AC_DTYPE_BF16;
+  const dim3 g1((unsigned)((max_n + kUsChunk * kUsWarps - 1) / (kUsChunk * kUsWarps)), nprob);
+  const dim3 g2((unsigned)((max_k + 3) / 4), nprob);
+  if (d == 64) {
+    if (bf) { k_usum<2, true><<<g1, 32 * kUsWarps, 0, st>>>(probs, d); k_ufin<2, true><<<g2, 128, 0, st>>>(probs, d, tol); }
+    else { k_usum<2, false><<<g1, 32 * kUsWarps, 0, st>>>(probs, d); k_ufin<2, false><<<g2, 128, 0, st>>>(probs, d, tol); }
+  } else {
+    if (bf) { k_usum<4, true><<<g1, 32 * kUsWarps, 0, st>>>(probs, d); k_ufin<4, true><<<g2, 128, 0, st>>>(probs, d, tol); }
+    else { k_usum<4, false><<<g1, 32 * kUsWarps, 0, st>>>(probs, d); k_ufin<4, false><<<g2, 128, 0, st>>>(probs, d, tol); }
+  }
+  AC_CHECK_LAUNCH("k_usum/k_ufin");
+  return AC_OK;
+}
+
+// Used for f32 points: their 256/512-byte rows make the gather efficient and
+// the member-order chains the longest; bf16 points (128-byte rows) measured
+// faster with the member-order kernel.
+static bool usum_ok(const ac_cluster_problem* host_probs, int nprob, int dtype, int d) {
+  if (g_update_mode != 0 || !host_probs || !(d == 64 || d == 128)) return false;
+  if (dtype != AC_DTYPE_F32) return false;
+  for (int p = 0; p < nprob; ++p)
+    if (!host_probs[p].csum || !host_probs[p].cabs || !host_probs[p].clsb) return false;
+  return true;
 }
 
 static int update_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d, int max_k,
@@ -1336,6 +1591,7 @@ static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int
   int order = AC_ORDER_SEQ;
   if (host_probs) order = host_probs[0].order;
   const bool inertia = !(lflags & AC_LLOYD_NO_INERTIA);
+  const bool split_update = usum_ok(host_probs, nprob, dtype, d);
   int rc = ac_lloyd_prepare(probs, nprob, dtype, d, max_n, max_k, stream);
   if (rc) return rc;
   int32_t* pinned = nullptr;
@@ -1346,7 +1602,9 @@ static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int
                           host_probs, st)))
       break;
     if ((rc = repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, inertia ? it : -1, 0, st))) break;
-    if ((rc = update_impl(probs, nprob, dtype, d, max_k, tol, 0, nullptr, st))) break;
+    if (split_update) rc = usum_update_impl(probs, nprob, dtype, d, max_n, max_k, tol, st);
+    else rc = update_impl(probs, nprob, dtype, d, max_k, tol, 0, nullptr, st);
+    if (rc) break;
     if (pinned && (it + 1) % poll_every == 0 && it + 1 < max_iter) {
       for (int p = 0; p < nprob; ++p)
         cudaMemcpyAsync(pinned + p, host_probs[p].status + AC_ST_ACTIVE, sizeof(int32_t),

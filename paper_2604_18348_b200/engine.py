@@ -111,6 +111,11 @@ class Batch:
         # (written by ac_lloyd_prepare), [3][n][D] per problem
         self.planes = (torch.empty(3 * N * D, dtype=torch.bfloat16, device=dev)
                        if self.dtype == L.DTYPE_F32 and D == 64 else None)
+        # split-chain centroid update workspaces (zeroed; the kernels re-zero)
+        fast = D in (64, 128)
+        self.csum = torch.zeros(K * D, dtype=torch.float64, device=dev) if fast else None
+        self.cabs = torch.zeros(K * D, dtype=F32, device=dev) if fast else None
+        self.clsb = torch.full((K * D,), 0x7F800000, dtype=I32, device=dev) if fast else None
         self.status = torch.zeros(P * L.STATUS_WORDS, dtype=I32, device=dev)
         desc = np.zeros(P, dtype=L.PROBLEM_DTYPE)
         self.n_off, self.k_off, self.t_off = [], [], []
@@ -140,6 +145,9 @@ class Batch:
             e["plan_k"] = 0
             e["dscratch"] = self.dscratch.data_ptr() + 8 * no
             e["planes"] = (self.planes.data_ptr() + 2 * 3 * no * D) if self.planes is not None else 0
+            e["csum"] = (self.csum.data_ptr() + 8 * ko * D) if self.csum is not None else 0
+            e["cabs"] = (self.cabs.data_ptr() + 4 * ko * D) if self.cabs is not None else 0
+            e["clsb"] = (self.clsb.data_ptr() + 4 * ko * D) if self.clsb is not None else 0
             e["n"] = self.ns[p]
             e["k"] = self.ks[p]
             e["order"] = self.orders[p]

@@ -124,3 +124,28 @@ def test_tc_assign_lloyd_parity(gpu, oracle):
     assert np.array_equal(a.centers, b.centers)
     assert a.n_iter == b.n_iter
     assert list(a.inertia_history) == list(b.inertia_history)
+
+
+@pytest.mark.parametrize("dtype,d,k", [("f32", 64, 65), ("bf16", 64, 100), ("f32", 128, 40),
+                                       ("bf16", 128, 128)])
+def test_split_chain_update_matches_member_order(gpu, dtype, d, k):
+    """k_usum/k_ufin (split f64 chains + exact f32 enclosure test, member-order
+    fallback) give the same Lloyd run as the member-order chains, bit for bit."""
+    from paper_2604_18348_b200 import _lib as L
+    from paper_2604_18348_b200 import engine as E
+    g = torch.Generator().manual_seed(d + k)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    xs = [(torch.randn(12000 + 777 * h, d, generator=g) * (1 + h)).to(tdt).cuda() for h in range(3)]
+    runs = []
+    for mode in (0, 1):
+        L.call("ac_set_update_mode", mode)
+        try:
+            ms = E.kmeans_batch(xs, [k] * 3, [1, 2, 3], 25, 1e-4)
+        finally:
+            L.call("ac_set_update_mode", 0)
+        torch.cuda.synchronize()
+        runs.append([(m.centers.clone(), m.labels.clone(), m.n_iter()) for m in ms])
+    for (c0, l0, n0), (c1, l1, n1) in zip(*runs):
+        assert n0 == n1
+        assert torch.equal(l0, l1)
+        assert torch.equal(c0, c1)
