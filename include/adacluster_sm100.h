@@ -65,6 +65,9 @@ extern "C" {
 #define AC_ASSIGN_MERGE 1   /* merge into existing (labels,best) with strict '<'
                                so earlier (lower-index) centres win ties        */
 #define AC_ASSIGN_ALL 2     /* ignore the per-problem 'active' flag            */
+#define AC_ASSIGN_LABELS_ONLY 4 /* labels exact, `best` exact only for rows
+                               that had near-ties (tensor-core path); the
+                               repair pass then recomputes exact distances  */
 
 /* ---------------------------------------------------------------------------
  * One clustering problem (one head, or one multi-stage round of one head).

@@ -423,7 +423,10 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const unsigned char* xsm = sm + s * SB;
         float best = INFINITY;
         int lbl = INT_MAX;
-        if (valid && ncand >= 1) {
+        if (valid && ncand == 1 && (prm.flags & AC_ASSIGN_LABELS_ONLY)) {
+          best = dmin;  // the label is decided; `best` approximate (see AC_ASSIGN_LABELS_ONLY)
+          lbl = c1;
+        } else if (valid && ncand >= 1) {
           best = exact_dist(xsm, f32in, r, cf32 + c1 * CF_STRIDE, xx, s_cc[c1]);
           lbl = c1;
           if (!(best < INFINITY)) { best = INFINITY; lbl = INT_MAX; }  // as `d < best` from +inf

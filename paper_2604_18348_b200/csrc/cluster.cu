@@ -420,6 +420,30 @@ k_post(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int iter,
   __shared__ long long s_far_i[32];
   __shared__ int s_scan[1024];
 
+  // labels-only assignment left approximate distances in `best`: the repair
+  // below needs the reference's exact ones, so recompute them (rare: only
+  // when some cluster is empty)
+  if (flags & AC_ASSIGN_LABELS_ONLY) {
+    if (tid == 0) s_empty = INT_MAX;
+    __syncthreads();
+    for (int c = tid; c < k; c += blockDim.x)
+      if (P.counts[c] == 0) atomicMin(&s_empty, c);
+    __syncthreads();
+    if (s_empty != INT_MAX) {
+      for (int64_t i = tid; i < n; i += blockDim.x) {
+        const int l = P.labels[i];
+        const float* crow = P.centers + (int64_t)l * d;
+        const int64_t base = i * d;
+        const bool halves = (i >= n - n % 4) && (l >= k - k % 4);
+        const float xc = ordered_dot([&](int t) { return ld_elem(P.x, dtype, base + t); },
+                                     [&](int t) { return crow[t]; }, d, P.order, halves);
+        P.best[i] = sq_dist(P.xx[i], xc, P.cc[l]);
+      }
+      __threadfence_block();
+    }
+    __syncthreads();
+  }
+
   // ---- empty-cluster repair: loop to a fixed point, at most k times ----
   for (int guard = 0; guard < k; ++guard) {
     if (tid == 0) s_empty = INT_MAX;
@@ -1591,6 +1615,12 @@ static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int
   int order = AC_ORDER_SEQ;
   if (host_probs) order = host_probs[0].order;
   const bool inertia = !(lflags & AC_LLOYD_NO_INERTIA);
+  // without inertia_history nothing but the (rare) empty-cluster repair reads
+  // `best`: the tensor-core assign may then skip the exact chain of rows with
+  // a single candidate, and the repair recomputes exact distances if needed
+  const int lo_flag = (!inertia && g_assign_mode != AC_ASSIGN_MODE_EXACT &&
+                       ac_host::assign_tc_eligible(host_probs, nprob, dtype, d, 0, order))
+                          ? AC_ASSIGN_LABELS_ONLY : 0;
   const bool split_update = usum_ok(host_probs, nprob, dtype, d);
   int rc = ac_lloyd_prepare(probs, nprob, dtype, d, max_n, max_k, stream);
   if (rc) return rc;
@@ -1598,10 +1628,11 @@ static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int
   if (poll_every > 0 && host_probs) cudaMallocHost(&pinned, sizeof(int32_t) * nprob);
   for (int it = 0; it < max_iter; ++it) {
     // ||c||^2 is current: prepare wrote it, then every centroid update does
-    if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, kAssignCcValid, order,
+    if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, kAssignCcValid | lo_flag, order,
                           host_probs, st)))
       break;
-    if ((rc = repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, inertia ? it : -1, 0, st))) break;
+    if ((rc = repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, inertia ? it : -1, lo_flag, st)))
+      break;
     if (split_update) rc = usum_update_impl(probs, nprob, dtype, d, max_n, max_k, tol, st);
     else rc = update_impl(probs, nprob, dtype, d, max_k, tol, 0, nullptr, st);
     if (rc) break;
@@ -1617,10 +1648,10 @@ static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int
   }
   if (pinned) cudaFreeHost(pinned);
   if (rc) return rc;
-  if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, AC_ASSIGN_ALL | kAssignCcValid,
-                        order, host_probs, st)))
+  if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0,
+                        AC_ASSIGN_ALL | kAssignCcValid | lo_flag, order, host_probs, st)))
     return rc;
-  return repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, -1, AC_ASSIGN_ALL, st);
+  return repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, -1, AC_ASSIGN_ALL | lo_flag, st);
 }
 
 extern "C" int ac_lloyd(const ac_cluster_problem* probs, int nprob, int dtype, int d,

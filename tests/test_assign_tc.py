@@ -149,3 +149,37 @@ def test_split_chain_update_matches_member_order(gpu, dtype, d, k):
         assert n0 == n1
         assert torch.equal(l0, l1)
         assert torch.equal(c0, c1)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_labels_only_lloyd_with_empty_cluster_repair(gpu, oracle, dtype):
+    """Lloyd without inertia (labels-only tensor-core assign, approximate
+    `best`) must still repair empty clusters exactly like the reference:
+    same labels, centres and iteration count as the exact-distance run and
+    as the oracle."""
+    import numpy as np
+    from paper_2604_18348_b200 import _lib as L
+    from paper_2604_18348_b200 import engine as E
+    g = torch.Generator().manual_seed(21)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    x = (torch.randn(6000, 64, generator=g) * 3).to(tdt)
+    init = x.float()[torch.randperm(6000, generator=g)[:40]].clone()
+    init[7] = 500.0   # far away: empty after the first assignment -> repair
+    init[23] = -500.0
+    res = []
+    for inertia in (True, False):
+        b = E.Batch([x.cuda()], [40], 25)
+        b.centers_of(0).copy_(init.cuda())
+        b.lloyd_range(0, 1, 25, 1e-4, inertia=inertia)
+        torch.cuda.synchronize()
+        st = b.status.view(b.P, L.STATUS_WORDS)[0].cpu().numpy()
+        res.append((b.labels.cpu().numpy(), b.centers_of(0).cpu().numpy(), int(st[L.ST_NITER]),
+                    int(st[L.ST_REPAIRS])))
+    (l0, c0, n0, r0), (l1, c1, n1, r1) = res
+    assert r0 > 0 and r0 == r1
+    assert n0 == n1
+    assert np.array_equal(l0, l1)
+    assert np.array_equal(c0, c1)
+    ref = oracle.lloyd(x.float().numpy(), init.numpy(), 25, 1e-4)
+    assert np.array_equal(l1, ref.assignments)
+    assert np.array_equal(c1, ref.centers)
