@@ -48,13 +48,12 @@ namespace asg {
 using namespace ac::tc;
 
 constexpr int BM = 128;     // rows per tile (== kAsgBM: shared tiling with the sort kernels)
-constexpr int DIM = 64;     // head_dim handled by this kernel
 constexpr int NBMAX = 128;  // centres per problem per launch (k - c_lo)
+constexpr int ATOM = BM * 128;  // one SW128 K-atom (64 bf16 columns) of a 128-row tile
 constexpr int MAXP = 32;    // problems per launch (tensor maps travel as kernel params)
 constexpr int THREADS = 320;
 constexpr int W_TMA = 0, W_MMA = 1, W_EPI0 = 2;
-constexpr int PL_BYTES = BM * DIM * 2;  // one bf16 plane of a tile (16 KB)
-constexpr int CF_STRIDE = DIM + 4;      // f32 centre rows, padded against bank conflicts
+constexpr int CF_STRIDE = 64 + 4;       // f32 centre rows (D = 64), padded against bank conflicts
 constexpr int QCAP = 64;                // per-warp queue of extra (row, centre) fix-up candidates
 constexpr int SMEM_MAX = 227 * 1024;
 constexpr float kPadE = 3.0e38f;        // e of the padding columns (never a candidate)
@@ -84,17 +83,20 @@ struct Params {
   Layout lay;
 };
 
-__host__ __device__ inline Layout make_layout(int dtype, int cap, int xs) {
+// D = 64: exact f32 centres in shared memory; D = 128: the exact centres
+// are re-joined from the -2c planes (no room for both)
+__host__ __device__ inline Layout make_layout(int dtype, int dim, int cap, int xs) {
   Layout l;
+  const int kb = dim / 64;
   l.np = dtype == AC_DTYPE_F32 ? 3 : 1;
   l.xs = xs;
-  l.stage_bytes = l.np * PL_BYTES;
+  l.stage_bytes = l.np * kb * ATOM;
   l.off_cp = l.xs * l.stage_bytes;
-  l.cp_bytes = cap * 128;
+  l.cp_bytes = kb * cap * 128;
   l.off_aa = l.off_cp + 3 * l.cp_bytes;
-  l.off_ab = l.off_aa + BM * 128;
-  l.off_cf = l.off_ab + l.cp_bytes;
-  l.off_cc = l.off_cf + cap * CF_STRIDE * 4;
+  l.off_ab = l.off_aa + BM * 32;   // aug operands: one K=16 step, SWIZZLE_32B
+  l.off_cf = l.off_ab + cap * 32;
+  l.off_cc = l.off_cf + (dim == 64 ? cap * CF_STRIDE * 4 : 0);
   l.off_hist = l.off_cc + NBMAX * 4;
   l.off_q = l.off_hist + 2 * NBMAX * 4;
   l.off_bar = l.off_q + 8 * QCAP * 8;
@@ -140,20 +142,23 @@ AC_DEV void join8(const uint4& h, const uint4& m, const uint4& l, float (&v)[8])
   }
 }
 
-// the reference's d for row r of the x tile and f32 centre row cf:
-// sequential fmaf chain from 0 (OpenBLAS general path), then sq_dist.
-// x comes from the tile's planes in shared memory (exactly joined).
-AC_DEV float exact_dist(const unsigned char* xsm, bool f32in, int r, const float* cf, float xx,
-                        float cc) {
+// the reference's d for row r of the x tile and centre c: sequential fmaf
+// chain from 0 (OpenBLAS general path), then sq_dist.  x comes from the
+// tile's planes in shared memory (exactly joined); c from the f32 rows
+// (D = 64) or re-joined from the -2c planes (exact, times -1/2).
+template <int DIM>
+AC_DEV float exact_dist(const unsigned char* xsm, bool f32in, int r, const float* cf,
+                        const unsigned char* cp, int cpb, int cap, int c, float xx, float cc) {
+  constexpr int PLB = BM * DIM * 2;
   float acc = 0.f;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int off = sw128(r, j);
+  for (int j = 0; j < DIM / 8; ++j) {
+    const int off = (j >> 3) * ATOM + sw128(r, j & 7);
     float xv[8];
     if (f32in) {
       join8(*reinterpret_cast<const uint4*>(xsm + off),
-            *reinterpret_cast<const uint4*>(xsm + PL_BYTES + off),
-            *reinterpret_cast<const uint4*>(xsm + 2 * PL_BYTES + off), xv);
+            *reinterpret_cast<const uint4*>(xsm + PLB + off),
+            *reinterpret_cast<const uint4*>(xsm + 2 * PLB + off), xv);
     } else {
       const uint4 w = *reinterpret_cast<const uint4*>(xsm + off);
       const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
@@ -163,9 +168,19 @@ AC_DEV float exact_dist(const unsigned char* xsm, bool f32in, int r, const float
         xv[2 * e + 1] = bf_hi(ww[e]);
       }
     }
-    const float4 c0 = *reinterpret_cast<const float4*>(cf + 8 * j);
-    const float4 c1 = *reinterpret_cast<const float4*>(cf + 8 * j + 4);
-    const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    float cv[8];
+    if constexpr (DIM == 64) {
+      const float4 c0 = *reinterpret_cast<const float4*>(cf + 8 * j);
+      const float4 c1 = *reinterpret_cast<const float4*>(cf + 8 * j + 4);
+      cv[0] = c0.x; cv[1] = c0.y; cv[2] = c0.z; cv[3] = c0.w;
+      cv[4] = c1.x; cv[5] = c1.y; cv[6] = c1.z; cv[7] = c1.w;
+    } else {
+      const int coff = (j >> 3) * cap * 128 + sw128(c, j & 7);
+      join8(*reinterpret_cast<const uint4*>(cp + coff), *reinterpret_cast<const uint4*>(cp + cpb + coff),
+            *reinterpret_cast<const uint4*>(cp + 2 * cpb + coff), cv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) cv[e] = __fmul_rn(-0.5f, cv[e]);
+    }
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc = __fmaf_rn(xv[e], cv[e], acc);
   }
@@ -182,8 +197,11 @@ AC_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 
+template <int DIM>
 __global__ void __launch_bounds__(THREADS, 1)
 k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __restrict__ probs) {
+  constexpr int KB = DIM / 64;           // SW128 K-atoms per row
+  constexpr int PL_BYTES = KB * ATOM;    // one bf16 plane of a tile
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -217,11 +235,11 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // aug A: rows of (1, 1, 1, 0, ...): picks up the 3-way split of ||c||^2
-  for (int e = tid; e < BM * 8; e += THREADS) {
-    const int r = e >> 3, j = e & 7;
+  for (int e = tid; e < BM * 2; e += THREADS) {
+    const int r = e >> 1, j = e & 1;
     uint4 w = make_uint4(0u, 0u, 0u, 0u);
     if (j == 0) w = make_uint4(0x3f803f80u, 0x00003f80u, 0u, 0u);  // bf16 1.0 = 0x3f80
-    *reinterpret_cast<uint4*>(aug_a + sw128(r, j)) = w;
+    *reinterpret_cast<uint4*>(aug_a + sw32(r, j)) = w;
   }
   if (warp == W_MMA) tmem_alloc(tmem_slot, 256);
   fence_proxy_async();
@@ -255,15 +273,18 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
     //      exact f32 rows and ||c||^2 (fix-up) ----
     if (tid == 0) *s_ccmax = 0;
     __syncthreads();
-    for (int e = tid; e < nbp * 8; e += THREADS) {
-      const int c = e >> 3, j = e & 7;
+    const int cap = CPB / (KB * 128);  // centre rows per plane atom
+    for (int e = tid; e < nbp * (DIM / 8); e += THREADS) {
+      const int c = e / (DIM / 8), j = e % (DIM / 8);
       float v[8];
       if (c < nb) {
         const float4* src = reinterpret_cast<const float4*>(P.centers + (int64_t)(c_lo + c) * DIM + 8 * j);
         const float4 a = src[0], b = src[1];
-        float4* dst = reinterpret_cast<float4*>(cf32 + c * CF_STRIDE + 8 * j);
-        dst[0] = a;
-        dst[1] = b;
+        if constexpr (DIM == 64) {
+          float4* dst = reinterpret_cast<float4*>(cf32 + c * CF_STRIDE + 8 * j);
+          dst[0] = a;
+          dst[1] = b;
+        }
         v[0] = -2.f * a.x; v[1] = -2.f * a.y; v[2] = -2.f * a.z; v[3] = -2.f * a.w;
         v[4] = -2.f * b.x; v[5] = -2.f * b.y; v[6] = -2.f * b.z; v[7] = -2.f * b.w;
       } else {
@@ -272,7 +293,7 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       }
       uint4 h, m, l;
       split8(v, h, m, l);
-      const int off = sw128(c, j);
+      const int off = (j >> 3) * cap * 128 + sw128(c, j & 7);
       *reinterpret_cast<uint4*>(cplanes + off) = h;
       *reinterpret_cast<uint4*>(cplanes + CPB + off) = m;
       *reinterpret_cast<uint4*>(cplanes + 2 * CPB + off) = l;
@@ -291,8 +312,8 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const __nv_bfloat16 h2 = __float2bfloat16_rn(__fsub_rn(r1, __bfloat162float(h1)));
         const uint32_t w0 = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
         const uint32_t w1 = (uint32_t)__bfloat16_as_ushort(h2);
-        *reinterpret_cast<uint4*>(aug_b + sw128(c, 0)) = make_uint4(w0, w1, 0u, 0u);
-        for (int j = 1; j < 8; ++j) *reinterpret_cast<uint4*>(aug_b + sw128(c, j)) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(aug_b + sw32(c, 0)) = make_uint4(w0, w1, 0u, 0u);
+        *reinterpret_cast<uint4*>(aug_b + sw32(c, 1)) = make_uint4(0u, 0u, 0u, 0u);
       }
     }
     fence_proxy_async();  // generic-proxy smem writes -> tensor-core (async proxy) reads
@@ -310,7 +331,10 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
           unsigned char* dst = sm + s * SB;
           mbar_expect_tx(xfull + s, SB);
           for (int q = 0; q < NP; ++q)
-            tma_load_2d(dst + q * PL_BYTES, &prm.x[p], 0, (int)(q * n) + row, xfull + s);
+#pragma unroll
+            for (int kb = 0; kb < KB; ++kb)
+              tma_load_2d(dst + q * PL_BYTES + kb * ATOM, &prm.x[p], kb * 64, (int)(q * n) + row,
+                          xfull + s);
         }
       }
       __syncwarp();
@@ -334,14 +358,16 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
           const uint32_t xa = smem_u32(sm + s * SB);
           const uint32_t d = tmem + (uint32_t)(b * 128);
           // ||c||^2 first (one K=16 step of the aug operands), then -2 x.c
-          umma_f16(d, sdesc(aa, 16, 1024), sdesc(ab, 16, 1024), idesc, 0u);
+          umma_f16(d, sdesc_sw32(aa), sdesc_sw32(ab), idesc, 0u);
 #pragma unroll
           for (int term = 0; term < 6; ++term) {
             if (term >= nterm) break;
 #pragma unroll
             for (int kk = 0; kk < DIM / 16; ++kk) {
-              const uint64_t ad = sdesc(xa + xi[term] * PL_BYTES + kk * 32, 16, 1024);
-              const uint64_t bd = sdesc(ca + ci[term] * CPB + kk * 32, 16, 1024);
+              const uint32_t kx = (kk >> 2) * ATOM + (kk & 3) * 32;
+              const uint32_t kc = (kk >> 2) * (CPB / KB) + (kk & 3) * 32;
+              const uint64_t ad = sdesc(xa + xi[term] * PL_BYTES + kx, 16, 1024);
+              const uint64_t bd = sdesc(ca + ci[term] * CPB + kc, 16, 1024);
               umma_f16(d, ad, bd, idesc, 1u);
             }
           }
@@ -427,7 +453,7 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
           best = dmin;  // the label is decided; `best` approximate (see AC_ASSIGN_LABELS_ONLY)
           lbl = c1;
         } else if (valid && ncand >= 1) {
-          best = exact_dist(xsm, f32in, r, cf32 + c1 * CF_STRIDE, xx, s_cc[c1]);
+          best = exact_dist<DIM>(xsm, f32in, r, cf32 + c1 * CF_STRIDE, cplanes, CPB, CPB / (KB * 128), c1, xx, s_cc[c1]);
           lbl = c1;
           if (!(best < INFINITY)) { best = INFINITY; lbl = INT_MAX; }  // as `d < best` from +inf
         }
@@ -456,7 +482,8 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
             for (int e2 = lane; e2 < total; e2 += 32) {
               const int src = (int)(qe[e2] >> 8), c = (int)(qe[e2] & 255u);
               const int64_t srow = (int64_t)tile * BM + q * 32 + src;
-              qr[e2] = exact_dist(xsm, f32in, q * 32 + src, cf32 + c * CF_STRIDE, P.xx[srow], s_cc[c]);
+              qr[e2] = exact_dist<DIM>(xsm, f32in, q * 32 + src, cf32 + c * CF_STRIDE, cplanes, CPB, CPB / (KB * 128), c,
+                                        P.xx[srow], s_cc[c]);
             }
             __syncwarp();
             for (int e2 = off; e2 < off + extra; ++e2) {  // ascending centre order
@@ -472,7 +499,7 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
                 const int c = ch * 32 + __ffs(m) - 1;
                 m &= m - 1;
                 if (c == c1) continue;
-                const float d = exact_dist(xsm, f32in, r, cf32 + c * CF_STRIDE, xx, s_cc[c]);
+                const float d = exact_dist<DIM>(xsm, f32in, r, cf32 + c * CF_STRIDE, cplanes, CPB, CPB / (KB * 128), c, xx, s_cc[c]);
                 if (d < best) { best = d; lbl = c; }
               }
             }
@@ -531,11 +558,18 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
 // ---------------------------------------------------------------------------
 namespace ac_host {
 
-// Can the tensor-core kernel take this batch?  (D = 64, general-path
-// accumulation order, <= 128 centres past c_lo, 16-byte aligned rows.)
+static int tc_cap(const ac_cluster_problem* host_probs, int nprob, int c_lo) {
+  int cap = 16;
+  for (int j = 0; j < nprob; ++j) cap = std::max(cap, (host_probs[j].k - c_lo + 15) & ~15);
+  return cap;
+}
+
+// Can the tensor-core kernel take this batch?  (D = 64 or 128, general-path
+// accumulation order, <= 128 centres past c_lo, 16-byte aligned rows, and
+// a shared-memory layout with at least one x stage.)
 bool assign_tc_eligible(const ac_cluster_problem* host_probs, int nprob, int dtype, int d,
                         int c_lo, int order) {
-  if (!host_probs || order != AC_ORDER_SEQ || d != ac::asg::DIM) return false;
+  if (!host_probs || order != AC_ORDER_SEQ || (d != 64 && d != 128)) return false;
   if (dtype != AC_DTYPE_F32 && dtype != AC_DTYPE_BF16) return false;
   for (int p = 0; p < nprob; ++p) {
     const ac_cluster_problem& P = host_probs[p];
@@ -546,31 +580,34 @@ bool assign_tc_eligible(const ac_cluster_problem* host_probs, int nprob, int dty
     if (dtype == AC_DTYPE_F32 && (!P.planes || (reinterpret_cast<uintptr_t>(P.planes) & 15)))
       return false;
   }
+  for (int p0 = 0; p0 < nprob; p0 += ac::asg::MAXP) {
+    const int cap = tc_cap(host_probs + p0, std::min(ac::asg::MAXP, nprob - p0), c_lo);
+    if (ac::asg::make_layout(dtype, d, cap, 1).smem > ac::asg::SMEM_MAX) return false;
+  }
   return true;
 }
 
 int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* host_probs,
-                     int nprob, int dtype, int c_lo, int flags, cudaStream_t st) {
+                     int nprob, int dtype, int d, int c_lo, int flags, cudaStream_t st) {
   using namespace ac::asg;
   static int sms = 0;
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute((const void*)k_assign_tc,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
-    if (e != cudaSuccess) return check_cuda(e, "k_assign_tc smem");
+    for (const void* f : {(const void*)k_assign_tc<64>, (const void*)k_assign_tc<128>}) {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+      if (e != cudaSuccess) return check_cuda(e, "k_assign_tc smem");
+    }
   }
   for (int p0 = 0; p0 < nprob; p0 += MAXP) {
     const int np = std::min(MAXP, nprob - p0);
     Params prm;
     memset(&prm, 0, sizeof(prm));
-    int cap = 16;
-    for (int j = 0; j < np; ++j)
-      cap = std::max(cap, (host_probs[p0 + j].k - c_lo + 15) & ~15);
+    const int cap = tc_cap(host_probs + p0, np, c_lo);
     int xs = 4;
-    while (xs > 1 && make_layout(dtype, cap, xs).smem > SMEM_MAX) --xs;
-    prm.lay = make_layout(dtype, cap, xs);
+    while (xs > 1 && make_layout(dtype, d, cap, xs).smem > SMEM_MAX) --xs;
+    prm.lay = make_layout(dtype, d, cap, xs);
     if (prm.lay.smem > SMEM_MAX) {
       set_error("k_assign_tc: shared-memory layout %d B exceeds the budget", prm.lay.smem);
       return AC_ERR_PARAM;
@@ -584,16 +621,20 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
       const ac_cluster_problem& P = host_probs[p0 + j];
       const int64_t tiles = (P.n + BM - 1) / BM;
       prm.tile0[j + 1] = prm.tile0[j] + (int)tiles;
-      // bf16 points: the tile itself; f32 points: the [3][n][64] planes
+      // bf16 points: the tile itself; f32 points: the [3][n][d] planes.
+      // Box = one 64-column SW128 atom; the kernel issues d/64 boxes per plane.
       const void* base = dtype == AC_DTYPE_F32 ? P.planes : P.x;
       const int64_t rows = (dtype == AC_DTYPE_F32 ? 3 : 1) * std::max<int64_t>(P.n, 1);
-      int rc = make_map_2d(&prm.x[j], base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, DIM, 64, BM);
+      int rc = make_map_2d(&prm.x[j], base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, d, 64, BM);
       if (rc) return rc;
     }
     const int total = prm.tile0[np];
     if (total == 0) continue;
     const int grid = std::min(total, sms);
-    k_assign_tc<<<grid, THREADS, prm.lay.smem, st>>>(prm, probs + p0);
+    if (d == 64)
+      k_assign_tc<64><<<grid, THREADS, prm.lay.smem, st>>>(prm, probs + p0);
+    else
+      k_assign_tc<128><<<grid, THREADS, prm.lay.smem, st>>>(prm, probs + p0);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return check_cuda(e, "k_assign_tc");
   }

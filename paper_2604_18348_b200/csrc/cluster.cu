@@ -1385,7 +1385,7 @@ namespace ac_host {
 bool assign_tc_eligible(const ac_cluster_problem* host_probs, int nprob, int dtype, int d,
                         int c_lo, int order);
 int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* host_probs,
-                     int nprob, int dtype, int c_lo, int flags, cudaStream_t st);
+                     int nprob, int dtype, int d, int c_lo, int flags, cudaStream_t st);
 }  // namespace ac_host
 
 namespace {
@@ -1464,13 +1464,13 @@ static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
   const bool tc_ok = ac_host::assign_tc_eligible(host_probs, nprob, dtype, d, c_lo, order);
   if (mode == AC_ASSIGN_MODE_TC && !tc_ok) {
     ac_host::set_error("assign: tensor-core path forced but the batch is not eligible "
-                       "(needs D=64, general order, k-c_lo<=128, host descriptors)");
+                       "(needs D=64/128, general order, k-c_lo<=128, host descriptors)");
     return AC_ERR_PARAM;
   }
   if (tc_ok && mode != AC_ASSIGN_MODE_EXACT) {
     if (!cc_valid) k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
     AC_CHECK_LAUNCH("k_center_sqnorm");
-    return ac_host::assign_tc_launch(probs, host_probs, nprob, dtype, c_lo, flags, st);
+    return ac_host::assign_tc_launch(probs, host_probs, nprob, dtype, d, c_lo, flags, st);
   }
   if (order == AC_ORDER_SEQ) {
     const size_t smem = assign_smem_bytes(d, max_k);

@@ -151,6 +151,18 @@ AC_DEV uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   d |= (uint64_t)2 << 61;  // SWIZZLE_128B
   return d;
 }
+// K-major SWIZZLE_32B operand (one K=16 bf16 step: 32-byte rows, 8-row
+// atoms of 256 B; 16-byte chunk j of row r at r*32 + ((j ^ (r>>2 & 1)) << 4))
+AC_DEV uint64_t sdesc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;  // SWIZZLE_32B
+  return d;
+}
+AC_DEV int sw32(int r, int j) { return r * 32 + ((j ^ ((r >> 2) & 1)) << 4); }
 // instruction descriptor: bf16 x bf16 -> f32, M x N, A K-major, B K- or MN-major
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool b_mn_major) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) |

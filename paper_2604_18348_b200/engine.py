@@ -110,7 +110,7 @@ class Batch:
         # f32 points: exact bf16 hi/mid/lo planes for the tensor-core assign
         # (written by ac_lloyd_prepare), [3][n][D] per problem
         self.planes = (torch.empty(3 * N * D, dtype=torch.bfloat16, device=dev)
-                       if self.dtype == L.DTYPE_F32 and D == 64 else None)
+                       if self.dtype == L.DTYPE_F32 and D in (64, 128) else None)
         # split-chain centroid update workspaces (zeroed; the kernels re-zero)
         fast = D in (64, 128)
         self.csum = torch.zeros(K * D, dtype=torch.float64, device=dev) if fast else None

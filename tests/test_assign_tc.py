@@ -49,25 +49,27 @@ def _compare(xs, centers, c_lo=0, merge_from=None):
     return a[3].cpu().numpy()
 
 
+@pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("n,k", [(200, 16), (127, 16), (128, 65), (129, 100), (5000, 128),
                                  (70000, 65), (70000, 100)])
-def test_tc_assign_random(gpu, dtype, n, k):
-    g = torch.Generator().manual_seed(n * 131 + k)
+def test_tc_assign_random(gpu, dtype, n, k, d):
+    g = torch.Generator().manual_seed(n * 131 + k + d)
     tdt = torch.float32 if dtype == "f32" else torch.bfloat16
-    x = (torch.randn(n, 64, generator=g) * 20).to(tdt).cuda()
+    x = (torch.randn(n, d, generator=g) * 20).to(tdt).cuda()
     idx = torch.randint(0, n, (k,), generator=g)
-    c = (x.float().cpu()[idx] + torch.randn(k, 64, generator=g) * 0.5).cuda()
+    c = (x.float().cpu()[idx] + torch.randn(k, d, generator=g) * 0.5).cuda()
     _compare([x], [c])
 
 
-def test_tc_assign_normalised_queries_batch(gpu):
+@pytest.mark.parametrize("d", [64, 128])
+def test_tc_assign_normalised_queries_batch(gpu, d):
     """Unit-norm f32 rows (the query side), several heads per launch."""
     g = torch.Generator().manual_seed(7)
     xs, cs = [], []
     for h in range(5):
         n = 3000 + 977 * h
-        x = torch.randn(n, 64, generator=g)
+        x = torch.randn(n, d, generator=g)
         x = (x / x.norm(dim=1, keepdim=True)).cuda()
         c = x[torch.randint(0, n, (65,), generator=g).cuda()] * 0.9
         xs.append(x.contiguous())
@@ -76,17 +78,18 @@ def test_tc_assign_normalised_queries_batch(gpu):
     assert (fix >= 0).all()
 
 
+@pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_tc_assign_exact_ties(gpu, dtype):
+def test_tc_assign_exact_ties(gpu, dtype, d):
     """Duplicated centres and rows exactly between two centres: the first
     index must win, exactly as numpy's argmin."""
     g = torch.Generator().manual_seed(3)
     tdt = torch.float32 if dtype == "f32" else torch.bfloat16
-    base = torch.randn(40, 64, generator=g) * 10
+    base = torch.randn(40, d, generator=g) * 10
     c = torch.cat([base, base[:10], base[5:15]])           # 60 centres, 20 duplicated
     mid = 0.5 * (base[:20] + base[20:40])                   # equidistant from pairs
     pts = torch.cat([mid.repeat(30, 1), base.repeat(20, 1),
-                     torch.randn(2000, 64, generator=g) * 10])
+                     torch.randn(2000, d, generator=g) * 10])
     x = pts.to(tdt).cuda().contiguous()
     fix = _compare([x], [c.cuda()])
     assert fix[0] > 0  # the duplicates must have gone through the exact fix-up
@@ -114,10 +117,11 @@ def test_tc_assign_merge(gpu):
     _compare([x], [both.contiguous()], c_lo=100, merge_from=(lab, best))
 
 
-def test_tc_assign_lloyd_parity(gpu, oracle):
+@pytest.mark.parametrize("d", [64, 128])
+def test_tc_assign_lloyd_parity(gpu, oracle, d):
     """A full Lloyd run through the tensor-core path equals the oracle."""
     rng = np.random.default_rng(1)
-    x = (rng.normal(size=(20000, 64)) * 5).astype(np.float32)
+    x = (rng.normal(size=(20000, d)) * 5).astype(np.float32)
     a = gpu.kmeans(x, 100, seed=4)
     b = oracle.kmeans(x, 100, 4)
     assert np.array_equal(a.assignments, b.assignments)
