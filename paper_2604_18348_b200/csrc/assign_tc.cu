@@ -150,8 +150,9 @@ template <int DIM>
 AC_DEV float exact_dist(const unsigned char* xsm, bool f32in, int r, const float* cf,
                         const unsigned char* cp, int cpb, int cap, int c, float xx, float cc) {
   constexpr int PLB = BM * DIM * 2;
+  constexpr int UNR = DIM == 64 ? 8 : 2;  // bounded register footprint at D = 128
   float acc = 0.f;
-#pragma unroll
+#pragma unroll UNR
   for (int j = 0; j < DIM / 8; ++j) {
     const int off = (j >> 3) * ATOM + sw128(r, j & 7);
     float xv[8];
@@ -444,21 +445,19 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         fence_before();
         mbar_arrive(aempty + b);
 
-        // exact chains: every row's first candidate on its own lane, then the
-        // warp's extra candidates (near-ties) spread over all 32 lanes
+        // exact chains, one per (row, candidate) that needs one, spread over
+        // all 32 lanes of the warp (a row whose single candidate is already
+        // decided needs none when only labels are asked for)
         const unsigned char* xsm = sm + s * SB;
+        const bool lonly = (prm.flags & AC_ASSIGN_LABELS_ONLY) != 0;
         float best = INFINITY;
         int lbl = INT_MAX;
-        if (valid && ncand == 1 && (prm.flags & AC_ASSIGN_LABELS_ONLY)) {
+        if (valid && ncand == 1 && lonly) {
           best = dmin;  // the label is decided; `best` approximate (see AC_ASSIGN_LABELS_ONLY)
           lbl = c1;
-        } else if (valid && ncand >= 1) {
-          best = exact_dist<DIM>(xsm, f32in, r, cf32 + c1 * CF_STRIDE, cplanes, CPB, CPB / (KB * 128), c1, xx, s_cc[c1]);
-          lbl = c1;
-          if (!(best < INFINITY)) { best = INFINITY; lbl = INT_MAX; }  // as `d < best` from +inf
         }
-        const int extra = (valid && ncand > 1) ? ncand - 1 : 0;
-        int incl = extra;
+        const int cnt = (valid && (ncand >= 2 || (ncand == 1 && !lonly))) ? ncand : 0;
+        int incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -466,40 +465,44 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         if (total > 0) {
-          const int off = incl - extra;
+          const int off = incl - cnt;
           if (total <= QCAP) {
-            int e = off;
+            if (cnt) {
+              int e = off;
 #pragma unroll
-            for (int ch = 0; ch < NBMAX / 32; ++ch) {
-              uint32_t m = mk[ch];
-              while (m) {
-                const int c = ch * 32 + __ffs(m) - 1;
-                m &= m - 1;
-                if (c != c1) qe[e++] = ((uint32_t)lane << 8) | (uint32_t)c;
+              for (int ch = 0; ch < NBMAX / 32; ++ch) {
+                uint32_t m = mk[ch];
+                while (m) {
+                  qe[e++] = ((uint32_t)lane << 8) | (uint32_t)(ch * 32 + __ffs(m) - 1);
+                  m &= m - 1;
+                }
               }
             }
             __syncwarp();
-            for (int e2 = lane; e2 < total; e2 += 32) {
-              const int src = (int)(qe[e2] >> 8), c = (int)(qe[e2] & 255u);
-              const int64_t srow = (int64_t)tile * BM + q * 32 + src;
-              qr[e2] = exact_dist<DIM>(xsm, f32in, q * 32 + src, cf32 + c * CF_STRIDE, cplanes, CPB, CPB / (KB * 128), c,
-                                        P.xx[srow], s_cc[c]);
+            for (int base = 0; base < total; base += 32) {
+              const int e2 = base + lane;
+              const uint32_t ent = e2 < total ? qe[e2] : 0u;
+              const int src = (int)(ent >> 8), c = (int)(ent & 255u);
+              const float xs = __shfl_sync(0xffffffffu, xx, src);
+              if (e2 < total)
+                qr[e2] = exact_dist<DIM>(xsm, f32in, q * 32 + src, cf32 + c * CF_STRIDE, cplanes, CPB,
+                                         CPB / (KB * 128), c, xs, s_cc[c]);
             }
             __syncwarp();
-            for (int e2 = off; e2 < off + extra; ++e2) {  // ascending centre order
+            for (int e2 = off; e2 < off + cnt; ++e2) {  // ascending centre order, first wins
               const float d = qr[e2];
               if (d < best) { best = d; lbl = (int)(qe[e2] & 255u); }
             }
             __syncwarp();
-          } else {  // very many near-ties in this warp: each lane walks its own
+          } else if (cnt) {  // very many near-ties in this warp: each lane walks its own
 #pragma unroll
             for (int ch = 0; ch < NBMAX / 32; ++ch) {
               uint32_t m = mk[ch];
               while (m) {
                 const int c = ch * 32 + __ffs(m) - 1;
                 m &= m - 1;
-                if (c == c1) continue;
-                const float d = exact_dist<DIM>(xsm, f32in, r, cf32 + c * CF_STRIDE, cplanes, CPB, CPB / (KB * 128), c, xx, s_cc[c]);
+                const float d = exact_dist<DIM>(xsm, f32in, r, cf32 + c * CF_STRIDE, cplanes, CPB,
+                                                CPB / (KB * 128), c, xx, s_cc[c]);
                 if (d < best) { best = d; lbl = c; }
               }
             }

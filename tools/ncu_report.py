@@ -5,7 +5,8 @@ rep = sys.argv[1]
 def run(*a):
     return subprocess.run(["ncu", "-i", rep, *a], capture_output=True, text=True).stdout
 raw = list(csv.reader(io.StringIO(run("--page", "raw", "--csv"))))
-h, v = raw[0], raw[2]
+IDX = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+h, v = raw[0], raw[2 + IDX]
 d = dict(zip(h, v))
 def g(k, default="?"):
     return d.get(k, default)
