@@ -136,6 +136,14 @@ int ac_gemm_order(int64_t m, int64_t n, int64_t d);
 int ac_l2norm(const void* x, int dtype, int64_t rows, int d, float* out,
               float* out_sqnorm, uint8_t* degenerate, void* stream);
 
+/* ac_l2norm that also writes, when planes != NULL, the exact bf16 hi/mid/lo
+ * split of the normalised rows as per-problem planes [3][prob_rows][d]
+ * (rows % prob_rows == 0; d = 64 or 128, 16-byte aligned buffers) -- the
+ * query-side prepare of ac_lloyd_ex fused into the normalisation pass.     */
+int ac_l2norm_ex(const void* x, int dtype, int64_t rows, int d, float* out,
+                 float* out_sqnorm, uint8_t* degenerate, void* planes, int64_t prob_rows,
+                 void* stream);
+
 /* pairwise ||x_i||^2 in f32 (clustering.py:71 `(x * x).sum(axis=1)`) */
 int ac_row_sqnorm(const void* x, int dtype, int64_t rows, int d, float* out,
                   void* stream);
@@ -165,6 +173,9 @@ int ac_lloyd(const ac_cluster_problem* probs, int nprob, int dtype, int d,
  * per-iteration inertia_history reduction (steady-state steps never read it;
  * labels, centres and n_iter are unaffected).                               */
 #define AC_LLOYD_NO_INERTIA 1
+/* the problems' xx (and, for f32 points, planes) are already current --
+ * written by ac_l2norm_ex in the same stream -- so the prepare pass skips them */
+#define AC_LLOYD_PREPARED 2
 int ac_lloyd_ex(const ac_cluster_problem* probs, int nprob, int dtype, int d,
                 int64_t max_n, int max_k, int max_iter, double tol, int flags,
                 const ac_cluster_problem* host_probs, void* stream);

@@ -26,6 +26,8 @@ ASSIGN_MERGE, ASSIGN_ALL = 1, 2
 ST_ACTIVE, ST_NITER, ST_DONE, ST_FLAGS, ST_KPP_STOP, ST_REPAIRS, ST_FIXUPS, ST_WIDE = range(8)
 ASSIGN_MODE_AUTO, ASSIGN_MODE_EXACT, ASSIGN_MODE_TC = range(3)
 LLOYD_NO_INERTIA = 1
+LLOYD_PREPARED = 2
+LLOYD_PREPARED = 2
 STATUS_WORDS = 8
 
 # struct layouts (must match the header; checked in tests/test_abi.py)
@@ -62,6 +64,7 @@ _SIGS = {
     "ac_pw_plan_build": [_I64, _P, _I64],
     "ac_gemm_order": [_I64, _I64, _I64],
     "ac_l2norm": [_P, _I, _I64, _I, _P, _P, _P, _P],
+    "ac_l2norm_ex": [_P, _I, _I64, _I, _P, _P, _P, _P, _I64, _P],
     "ac_row_sqnorm": [_P, _I, _I64, _I, _P, _P],
     "ac_kmeanspp": [_P, _I, _I, _I, _I64, _I, _P, _P],
     "ac_lloyd": [_P, _I, _I, _I, _I64, _I, _I, _D, _I, _P, _P],

@@ -112,6 +112,161 @@ k_l2norm(const void* __restrict__ x, int dtype, int64_t rows, int d, float* __re
   }
 }
 
+// ---- fast path for D = 64 / 128 (16-byte aligned rows) --------------------
+// 64 rows per 256-thread block staged as f32 [64][D+8] with 16-byte loads;
+// 8 lanes per row each run one of numpy's 8 pairwise accumulators
+// (pw_leaf: r_j = sum_m a[j+8m] in order) and the shuffle tree combines them
+// as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) -- same operations, same bits.
+// The stride D+8 puts the 4 rows x 8 lanes of one access on 32 banks.
+constexpr int kRowsV = 64;
+
+template <int D>
+AC_DEV void stage_rows_v(const void* __restrict__ x, int dtype, int64_t row0, int nr, float* s) {
+  constexpr int LD = D + 8;
+  if (reinterpret_cast<uintptr_t>(x) & 15) {  // unaligned rows: element loads
+    for (int e = threadIdx.x; e < nr * D; e += blockDim.x)
+      s[(e / D) * LD + e % D] = ld_elem(x, dtype, row0 * D + e);
+    return;
+  }
+  if (dtype == AC_DTYPE_BF16) {
+    const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(x) + row0 * D);
+    for (int c = threadIdx.x; c < nr * (D / 8); c += blockDim.x) {
+      const int r = c / (D / 8), j = c % (D / 8);
+      const uint4 w = __ldg(src + c);
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+      float4* dst = reinterpret_cast<float4*>(s + r * LD + 8 * j);
+      dst[0] = make_float4(__uint_as_float(ww[0] << 16), __uint_as_float(ww[0] & 0xffff0000u),
+                           __uint_as_float(ww[1] << 16), __uint_as_float(ww[1] & 0xffff0000u));
+      dst[1] = make_float4(__uint_as_float(ww[2] << 16), __uint_as_float(ww[2] & 0xffff0000u),
+                           __uint_as_float(ww[3] << 16), __uint_as_float(ww[3] & 0xffff0000u));
+    }
+  } else {
+    const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + row0 * D);
+    for (int c = threadIdx.x; c < nr * (D / 4); c += blockDim.x) {
+      const int r = c / (D / 4), j = c % (D / 4);
+      *reinterpret_cast<float4*>(s + r * LD + 4 * j) = __ldg(src + c);
+    }
+  }
+}
+
+// combine the 8 accumulators of a lane group (lanes 8g..8g+7) in numpy's order
+AC_DEV float pw8_combine(float r) {
+  r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+  r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+  return __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+}
+
+template <int D>
+AC_DEV float row_sq_pw8(const float* srow, int j) {
+  float r = __fmul_rn(srow[j], srow[j]);
+#pragma unroll
+  for (int m = 1; m < D / 8; ++m) r = __fadd_rn(r, __fmul_rn(srow[j + 8 * m], srow[j + 8 * m]));
+  return pw8_combine(r);
+}
+
+// exact bf16 hi/mid/lo split of 8 staged values -> planes[q][row][8j..8j+7]
+AC_DEV void write_planes8(const float* v, __nv_bfloat16* pl, int64_t plane, int64_t o) {
+  uint32_t h[4], m[4], l[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    uint32_t hh[2], mm[2], ll[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const float a = v[2 * e + u];
+      const __nv_bfloat16 b0 = __float2bfloat16_rn(a);
+      const float r1 = __fsub_rn(a, __bfloat162float(b0));
+      const __nv_bfloat16 b1 = __float2bfloat16_rn(r1);
+      const __nv_bfloat16 b2 = __float2bfloat16_rn(__fsub_rn(r1, __bfloat162float(b1)));
+      hh[u] = __bfloat16_as_ushort(b0);
+      mm[u] = __bfloat16_as_ushort(b1);
+      ll[u] = __bfloat16_as_ushort(b2);
+    }
+    h[e] = hh[0] | (hh[1] << 16);
+    m[e] = mm[0] | (mm[1] << 16);
+    l[e] = ll[0] | (ll[1] << 16);
+  }
+  *reinterpret_cast<uint4*>(pl + o) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(pl + plane + o) = make_uint4(m[0], m[1], m[2], m[3]);
+  *reinterpret_cast<uint4*>(pl + 2 * plane + o) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// One block of rows [row0, row0+nr): optional l2 normalisation (K1
+// semantics of k_l2norm), ||row||^2 of the (normalised) rows, the f32 rows
+// (when normalising) and their bf16 planes.  Plane rows are addressed per
+// problem: global row g -> problem g / prob_rows, [3][prob_rows][D] each.
+template <int D>
+AC_DEV void rows_block_v(const void* __restrict__ x, int dtype, int64_t row0, int nr, bool normalise,
+                         float* __restrict__ out, float* __restrict__ out_sq,
+                         uint8_t* __restrict__ degenerate, __nv_bfloat16* __restrict__ planes,
+                         int64_t prob_rows, float* s) {
+  constexpr int LD = D + 8;
+  stage_rows_v<D>(x, dtype, row0, nr, s);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, j = lane & 7;
+  const int nwarps = blockDim.x >> 5;
+  for (int rb = warp * 4; rb < nr; rb += nwarps * 4) {
+    const int r = rb + (lane >> 3);
+    const bool ok = r < nr;
+    float* srow = s + (ok ? r : 0) * LD;
+    float sq = row_sq_pw8<D>(srow, j);
+    if (normalise) {
+      const float norm = __fsqrt_rn(sq);
+      const bool degen = norm < 1e-12f;                         // DEGENERATE_NORM
+      const bool unit = fabsf(__fsub_rn(norm, 1.0f)) <= 2e-6f;  // already unit
+      const float safe = (degen || unit) ? 1.0f : norm;
+      float acc = 0.f;
+#pragma unroll
+      for (int m = 0; m < D / 8; ++m) {
+        const float v = degen ? 0.f : __fdiv_rn(srow[j + 8 * m], safe);
+        if (ok) srow[j + 8 * m] = v;
+        acc = m == 0 ? __fmul_rn(v, v) : __fadd_rn(acc, __fmul_rn(v, v));
+      }
+      sq = pw8_combine(acc);
+      if (ok && j == 0 && degenerate) degenerate[row0 + r] = degen ? 1 : 0;
+    }
+    if (ok && j == 0 && out_sq) out_sq[row0 + r] = sq;
+  }
+  __syncthreads();
+  if (normalise && out) {
+    float4* dst = reinterpret_cast<float4*>(out + row0 * D);
+    for (int c = threadIdx.x; c < nr * (D / 4); c += blockDim.x) {
+      const int r = c / (D / 4), jj = c % (D / 4);
+      dst[c] = *reinterpret_cast<const float4*>(s + r * LD + 4 * jj);
+    }
+  }
+  if (planes && !(reinterpret_cast<uintptr_t>(planes) & 15)) {
+    for (int c = threadIdx.x; c < nr * (D / 8); c += blockDim.x) {
+      const int r = c / (D / 8), jj = c % (D / 8);
+      const int64_t g = row0 + r, p = g / prob_rows, i = g - p * prob_rows;
+      const int64_t plane = prob_rows * D;
+      write_planes8(s + r * LD + 8 * jj, planes + 3 * p * plane, plane, i * D + 8 * jj);
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+k_l2norm_v(const void* __restrict__ x, int dtype, int64_t rows, float* __restrict__ out,
+           float* __restrict__ out_sq, uint8_t* __restrict__ degenerate,
+           __nv_bfloat16* __restrict__ planes, int64_t prob_rows) {
+  extern __shared__ float nsm[];
+  const int64_t row0 = (int64_t)blockIdx.x * kRowsV;
+  const int nr = (int)min((int64_t)kRowsV, rows - row0);
+  rows_block_v<D>(x, dtype, row0, nr, true, out, out_sq, degenerate, planes, prob_rows, nsm);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+k_problem_xx_v(const ac_cluster_problem* __restrict__ probs, int dtype) {
+  extern __shared__ float nsm[];
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  const int64_t row0 = (int64_t)blockIdx.x * kRowsV;
+  if (row0 >= P.n) return;
+  const int nr = (int)min((int64_t)kRowsV, P.n - row0);
+  __nv_bfloat16* pl = (P.planes && dtype == AC_DTYPE_F32) ? reinterpret_cast<__nv_bfloat16*>(P.planes) : nullptr;
+  rows_block_v<D>(P.x, dtype, row0, nr, false, nullptr, P.xx, nullptr, pl, P.n, nsm);
+}
+
 // center squared norms cc[c] for problem blockIdx.y
 __global__ void k_center_sqnorm(const ac_cluster_problem* __restrict__ probs, int d,
                                 int c_lo) {
@@ -1421,10 +1576,38 @@ extern "C" int ac_row_sqnorm(const void* x, int dtype, int64_t rows, int d, floa
   return AC_OK;
 }
 
-extern "C" int ac_l2norm(const void* x, int dtype, int64_t rows, int d, float* out,
-                         float* out_sq, uint8_t* degenerate, void* stream) {
+static bool rows_v_ok(const void* x, int dtype, int d) {
+  return (d == 64 || d == 128) && (dtype == AC_DTYPE_F32 || dtype == AC_DTYPE_BF16) &&
+         !(reinterpret_cast<uintptr_t>(x) & 15);
+}
+
+static size_t rows_v_smem(int d) { return sizeof(float) * kRowsV * (d + 8); }
+
+extern "C" int ac_l2norm_ex(const void* x, int dtype, int64_t rows, int d, float* out,
+                            float* out_sq, uint8_t* degenerate, void* planes, int64_t prob_rows,
+                            void* stream) {
   if (rows < 0 || d < 1) { ac_host::set_error("ac_l2norm: bad shape"); return AC_ERR_DIM; }
   if (rows == 0) return AC_OK;
+  const bool fast = rows_v_ok(x, dtype, d) && !(reinterpret_cast<uintptr_t>(out) & 15) &&
+                    !(reinterpret_cast<uintptr_t>(planes) & 15);
+  if (planes && (!fast || prob_rows <= 0 || rows % prob_rows)) {
+    ac_host::set_error("ac_l2norm_ex: planes need d=64/128, aligned rows and rows %% prob_rows == 0");
+    return AC_ERR_PARAM;
+  }
+  if (fast) {
+    const size_t smem = rows_v_smem(d);
+    const void* fn = d == 64 ? (const void*)k_l2norm_v<64> : (const void*)k_l2norm_v<128>;
+    int rc = set_smem(fn, smem);
+    if (rc) return rc;
+    const unsigned grid = (unsigned)((rows + kRowsV - 1) / kRowsV);
+    __nv_bfloat16* pl = reinterpret_cast<__nv_bfloat16*>(planes);
+    if (d == 64)
+      k_l2norm_v<64><<<grid, 256, smem, S(stream)>>>(x, dtype, rows, out, out_sq, degenerate, pl, prob_rows);
+    else
+      k_l2norm_v<128><<<grid, 256, smem, S(stream)>>>(x, dtype, rows, out, out_sq, degenerate, pl, prob_rows);
+    AC_CHECK_LAUNCH("k_l2norm_v");
+    return AC_OK;
+  }
   const size_t smem = sizeof(float) * kNormRows * (d + 1);
   int rc = set_smem((const void*)k_l2norm, smem);
   if (rc) return rc;
@@ -1434,18 +1617,41 @@ extern "C" int ac_l2norm(const void* x, int dtype, int64_t rows, int d, float* o
   return AC_OK;
 }
 
-extern "C" int ac_lloyd_prepare(const ac_cluster_problem* probs, int nprob, int dtype, int d,
-                                int64_t max_n, int max_k, void* stream) {
+extern "C" int ac_l2norm(const void* x, int dtype, int64_t rows, int d, float* out,
+                         float* out_sq, uint8_t* degenerate, void* stream) {
+  return ac_l2norm_ex(x, dtype, rows, d, out, out_sq, degenerate, nullptr, 0, stream);
+}
+
+static int prepare_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d, int64_t max_n,
+                        int max_k, bool rows_done, void* stream) {
   if (nprob <= 0) return AC_OK;
+  const bool rows_fast = (d == 64 || d == 128) && (dtype == AC_DTYPE_F32 || dtype == AC_DTYPE_BF16);
   k_status_init<<<(nprob + 127) / 128, 128, 0, S(stream)>>>(probs, nprob);
-  const size_t xsm = sizeof(float) * kNormRows * (d + 1);
-  int rc = set_smem((const void*)k_problem_xx, xsm);
-  if (rc) return rc;
-  k_problem_xx<<<dim3((unsigned)((max_n + kNormRows - 1) / kNormRows), nprob), kNormRows, xsm,
-                 S(stream)>>>(probs, dtype, d);
+  if (rows_done) {
+    // ||x||^2 (and the f32 planes) are current: written by ac_l2norm_ex
+  } else if (rows_fast) {
+    const size_t xsm = rows_v_smem(d);
+    const void* fn = d == 64 ? (const void*)k_problem_xx_v<64> : (const void*)k_problem_xx_v<128>;
+    int rc = set_smem(fn, xsm);
+    if (rc) return rc;
+    const dim3 grid((unsigned)((max_n + kRowsV - 1) / kRowsV), nprob);
+    if (d == 64) k_problem_xx_v<64><<<grid, 256, xsm, S(stream)>>>(probs, dtype);
+    else k_problem_xx_v<128><<<grid, 256, xsm, S(stream)>>>(probs, dtype);
+  } else {
+    const size_t xsm = sizeof(float) * kNormRows * (d + 1);
+    int rc = set_smem((const void*)k_problem_xx, xsm);
+    if (rc) return rc;
+    k_problem_xx<<<dim3((unsigned)((max_n + kNormRows - 1) / kNormRows), nprob), kNormRows, xsm,
+                   S(stream)>>>(probs, dtype, d);
+  }
   k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, S(stream)>>>(probs, d, 0);
   AC_CHECK_LAUNCH("ac_lloyd_prepare");
   return AC_OK;
+}
+
+extern "C" int ac_lloyd_prepare(const ac_cluster_problem* probs, int nprob, int dtype, int d,
+                                int64_t max_n, int max_k, void* stream) {
+  return prepare_impl(probs, nprob, dtype, d, max_n, max_k, false, stream);
 }
 
 // `generic` is decided per batch by the host (every problem of a batch shares
@@ -1622,7 +1828,8 @@ static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int
                        ac_host::assign_tc_eligible(host_probs, nprob, dtype, d, 0, order))
                           ? AC_ASSIGN_LABELS_ONLY : 0;
   const bool split_update = usum_ok(host_probs, nprob, dtype, d);
-  int rc = ac_lloyd_prepare(probs, nprob, dtype, d, max_n, max_k, stream);
+  int rc = prepare_impl(probs, nprob, dtype, d, max_n, max_k, (lflags & AC_LLOYD_PREPARED) != 0,
+                        stream);
   if (rc) return rc;
   int32_t* pinned = nullptr;
   if (poll_every > 0 && host_probs) cudaMallocHost(&pinned, sizeof(int32_t) * nprob);

@@ -200,14 +200,16 @@ class Batch:
                    max(self.ns[g0:g1]), max(self.kcaps[g0:g1]), int(max_iter), float(tol),
                    int(poll_every), self.desc.ctypes.data + g0 * isz, L.stream_ptr())
 
-    def lloyd_range(self, g0: int, g1: int, max_iter: int, tol: float, inertia: bool = True):
+    def lloyd_range(self, g0: int, g1: int, max_iter: int, tol: float, inertia: bool = True,
+                    prepared: bool = False):
         """Lloyd on problems [g0, g1) of the batch (current stream);
-        ``inertia=False`` skips the inertia_history reductions."""
+        ``inertia=False`` skips the inertia_history reductions; ``prepared``:
+        xx/planes were written by ac_l2norm_ex (see SteadyStep)."""
         isz = self.desc.dtype.itemsize
+        flags = (0 if inertia else L.LLOYD_NO_INERTIA) | (L.LLOYD_PREPARED if prepared else 0)
         L.call("ac_lloyd_ex", self.dev.data_ptr() + g0 * isz, g1 - g0, self.dtype, self.D,
                max(self.ns[g0:g1]), max(self.kcaps[g0:g1]), int(max_iter), float(tol),
-               0 if inertia else L.LLOYD_NO_INERTIA, self.desc.ctypes.data + g0 * isz,
-               L.stream_ptr())
+               flags, self.desc.ctypes.data + g0 * isz, L.stream_ptr())
 
     def l2_group(self, budget: float = 48e6) -> int:
         """Problems per block so that a block's points fit in ~`budget` bytes of L2."""

@@ -173,14 +173,16 @@ class SteadyStep:
         if host is not None:
             self.Q.copy_(host[0], non_blocking=True)
         s = L.stream_ptr()
-        L.call("ac_l2norm", self.Q.data_ptr(), self.dt, H * Ln, D, self.qn.data_ptr(), 0,
-               self.qdeg.data_ptr(), s)
+        # normalisation + the query Batch's prepare (xx, f32 planes) in one pass
+        L.call("ac_l2norm_ex", self.Q.data_ptr(), self.dt, H * Ln, D, self.qn.data_ptr(),
+               qb.xx.data_ptr(), self.qdeg.data_ptr(),
+               qb.planes.data_ptr() if qb.planes is not None else 0, Ln, s)
         self.fork.record(main)
         for i, (h0, h1) in enumerate(blocks):
             qs = self.streams[2 * i + 1]
             qs.wait_event(self.fork)
             with torch.cuda.stream(qs):
-                qb.lloyd_range(h0, h1, p.max_iter, p.tol, inertia=False)
+                qb.lloyd_range(h0, h1, p.max_iter, p.tol, inertia=False, prepared=True)
                 self.joins[2 * i + 1].record(qs)
         if host is not None:
             self.K.copy_(host[1], non_blocking=True)
