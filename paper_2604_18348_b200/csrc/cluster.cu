@@ -1769,7 +1769,8 @@ static int usum_update_impl(const ac_cluster_problem* probs, int nprob, int dtyp
 // faster with the member-order kernel.
 static bool usum_ok(const ac_cluster_problem* host_probs, int nprob, int dtype, int d) {
   if (g_update_mode != 0 || !host_probs || !(d == 64 || d == 128)) return false;
-  if (dtype != AC_DTYPE_F32) return false;
+  static const int bf_ok = getenv("AC_USUM_BF16") ? atoi(getenv("AC_USUM_BF16")) : 0;
+  if (dtype != AC_DTYPE_F32 && !(dtype == AC_DTYPE_BF16 && bf_ok)) return false;
   for (int p = 0; p < nprob; ++p)
     if (!host_probs[p].csum || !host_probs[p].cabs || !host_probs[p].clsb) return false;
   return true;

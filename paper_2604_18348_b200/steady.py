@@ -145,11 +145,23 @@ class SteadyStep:
         self.split = max(1, min(split, H))
         self.hb = (H + self.split - 1) // self.split
         nblk = (H + self.hb - 1) // self.hb
-        self.streams = [torch.cuda.Stream() for _ in range(2 * nblk)]
+        # pipelined tails (AC_STEADY_PIPE=1; measured slower at split 2-6, off):
+        # block i's selection + attention start as soon as its
+        # own chains finish, overlapping later blocks' clustering; earlier
+        # blocks get higher stream priority so that they finish first
+        self.pipe = int(os.environ.get("AC_STEADY_PIPE", "0")) != 0 and nblk > 1
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
+            else (0, -1)
+        prios = [max(hi, lo - (nblk - 1 - i)) if self.pipe else 0 for i in range(nblk)]
+        self.streams = [torch.cuda.Stream(priority=prios[i // 2]) for i in range(2 * nblk)]
         self.fork = torch.cuda.Event()
         self.fork_k = torch.cuda.Event()
+        self.fork_v = torch.cuda.Event()
         self.host_graphs = {}
         self.joins = [torch.cuda.Event() for _ in range(2 * nblk)]
+        self.tails = [torch.cuda.Event() for _ in range(nblk)]
+        self.ev_blk = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]
+                       for _ in range(nblk)]
 
     # ------------------------------------------------------------------
     def _enqueue(self, host=None):
@@ -197,31 +209,60 @@ class SteadyStep:
                 self.joins[2 * i].record(ks)
         if host is not None:
             self.V.copy_(host[2], non_blocking=True)
-        for i in range(2 * len(blocks)):
-            main.wait_event(self.joins[i])
-        s = L.stream_ptr()
-        L.call("ac_segment_mean", self.reps_desc.data_ptr(), H, L.DTYPE_F32, D, self.gq,
-               self.reps_ptrs.data_ptr(), s)
-        L.call("ac_envelopes", self.env_desc.data_ptr(), H, self.dt, D, kb.max_k,
-               self.pmax.data_ptr(), self.pmin.data_ptr(), s)
-        L.call("ac_select", self.sel_desc.data_ptr(), H, D, self.scorer, self.gq, kb.max_k,
-               self.stride, s)
-        L.call("ac_permute_rows_heads", self.K.data_ptr(), self.dt, D, self.kperm.data_ptr(),
-               Ln, H, self.kp.data_ptr(), s)
-        L.call("ac_permute_rows_heads", self.V.data_ptr(), self.dt, D, self.kperm.data_ptr(),
-               Ln, H, self.vp.data_ptr(), s)
-        L.call("ac_build_q_layout", self.Q.data_ptr(), self.dt, D, Ln, H, self.qperm.data_ptr(),
-               self.qstarts.data_ptr(), self.qcounts.data_ptr(), self.qlab.data_ptr(),
-               self.gq_t.data_ptr(), self.gq, self.nruns.data_ptr(), self.stride,
-               self.qp.data_ptr(), self.qidx.data_ptr(), self.qp_cap, self.items.data_ptr(),
-               self.item_cap, self.item_rows, s)
-        self.ev[1].record()
-        L.call("ac_sparse_attention", self.qp.data_ptr(), H * self.qp_cap, self.qidx.data_ptr(),
-               self.kp.data_ptr(), self.vp.data_ptr(), self.dt, D, Ln, H, self.items.data_ptr(),
-               H * self.item_cap, self.runs.data_ptr(), self.scale, self.out.data_ptr(), self.odt, s)
-        self.ev[2].record()
+        if self.pipe:
+            self.fork_v.record(main)
+            for i, (h0, h1) in enumerate(blocks):
+                ks = self.streams[2 * i]
+                ks.wait_event(self.joins[2 * i + 1])
+                ks.wait_event(self.fork_v)
+                with torch.cuda.stream(ks):
+                    self._tail(h0, h1, self.ev_blk[i])
+                    self.tails[i].record(ks)
+            for i in range(len(blocks)):
+                main.wait_event(self.tails[i])
+            self.ev[1].record()
+            self.ev[2].record()
+        else:
+            for i in range(2 * len(blocks)):
+                main.wait_event(self.joins[i])
+            self._tail(0, H, self.ev[1:3])
         if host is not None:
             host[3].copy_(self.out, non_blocking=True)
+
+    def _tail(self, h0: int, h1: int, evs):
+        """Selection, layouts and attention of heads [h0, h1) on the current
+        stream (descriptor arrays and buffers offset to the head range)."""
+        Ln, D = self.L, self.D
+        nb = h1 - h0
+        kb = self.kb
+        s = L.stream_ptr()
+        psz = 8
+        esz = self.K.element_size()
+        L.call("ac_segment_mean", self.reps_desc.data_ptr() + h0 * L.PROBLEM_DTYPE.itemsize, nb,
+               L.DTYPE_F32, D, self.gq, self.reps_ptrs.data_ptr() + h0 * psz, s)
+        L.call("ac_envelopes", self.env_desc.data_ptr() + h0 * L.PROBLEM_DTYPE.itemsize, nb, self.dt, D,
+               kb.max_k, self.pmax.data_ptr() + h0 * psz, self.pmin.data_ptr() + h0 * psz, s)
+        L.call("ac_select", self.sel_desc.data_ptr() + h0 * L.SELECT_DTYPE.itemsize, nb, D, self.scorer,
+               self.gq, kb.max_k, self.stride, s)
+        hoff = h0 * Ln * D * esz
+        L.call("ac_permute_rows_heads", self.K.data_ptr() + hoff, self.dt, D, self.kperm[h0].data_ptr(),
+               Ln, nb, self.kp.data_ptr() + hoff, s)
+        L.call("ac_permute_rows_heads", self.V.data_ptr() + hoff, self.dt, D, self.kperm[h0].data_ptr(),
+               Ln, nb, self.vp.data_ptr() + hoff, s)
+        qp = self.qp[h0 * self.qp_cap:]
+        qidx = self.qidx[h0 * (self.qp_cap + self.gq):]
+        items = self.items[h0 * self.item_cap * L.ITEM_DTYPE.itemsize:]
+        L.call("ac_build_q_layout", self.Q.data_ptr() + hoff, self.dt, D, Ln, nb, self.qperm[h0].data_ptr(),
+               self.qstarts[h0].data_ptr(), self.qcounts[h0].data_ptr(), self.qlab[h0].data_ptr(),
+               self.gq_t[h0:].data_ptr(), self.gq, self.nruns[h0].data_ptr(), self.stride,
+               qp.data_ptr(), qidx.data_ptr(), self.qp_cap, items.data_ptr(),
+               self.item_cap, self.item_rows, s)
+        evs[0].record()
+        L.call("ac_sparse_attention", qp.data_ptr(), nb * self.qp_cap, qidx.data_ptr(),
+               self.kp.data_ptr() + hoff, self.vp.data_ptr() + hoff, self.dt, D, Ln, nb, items.data_ptr(),
+               nb * self.item_cap, self.runs[h0].data_ptr(), self.scale,
+               self.out[h0].data_ptr(), self.odt, s)
+        evs[1].record()
 
     def _capture(self, host=None):
         # one eager run on a side stream (lazy kernel attributes, workspaces),
@@ -271,6 +312,12 @@ class SteadyStep:
     def last_times_ms(self) -> dict:
         """Device time of the last step's phases (synchronises)."""
         self.ev[2].synchronize()
+        if self.pipe:
+            # per-block attention launches overlap later blocks' clustering:
+            # report their summed device time (on the launching streams)
+            att = sum(a.elapsed_time(b) for a, b in self.ev_blk)
+            return {"cluster_select_layout": self.ev[0].elapsed_time(self.ev[1]) - att,
+                    "attention": att}
         return {"cluster_select_layout": self.ev[0].elapsed_time(self.ev[1]),
                 "attention": self.ev[1].elapsed_time(self.ev[2])}
 
