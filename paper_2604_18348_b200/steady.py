@@ -145,26 +145,40 @@ class SteadyStep:
         self.split = max(1, min(split, H))
         self.hb = (H + self.split - 1) // self.split
         nblk = (H + self.hb - 1) // self.hb
-        # pipelined tails (AC_STEADY_PIPE=1; measured slower at split 2-6, off):
-        # block i's selection + attention start as soon as its
-        # own chains finish, overlapping later blocks' clustering; earlier
-        # blocks get higher stream priority so that they finish first
-        self.pipe = int(os.environ.get("AC_STEADY_PIPE", "0")) != 0 and nblk > 1
-        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
-            else (0, -1)
-        prios = [max(hi, lo - (nblk - 1 - i)) if self.pipe else 0 for i in range(nblk)]
-        self.streams = [torch.cuda.Stream(priority=prios[i // 2]) for i in range(2 * nblk)]
+        self.streams = [torch.cuda.Stream() for _ in range(2 * nblk)]
         self.fork = torch.cuda.Event()
         self.fork_k = torch.cuda.Event()
         self.fork_v = torch.cuda.Event()
         self.host_graphs = {}
         self.joins = [torch.cuda.Event() for _ in range(2 * nblk)]
-        self.tails = [torch.cuda.Event() for _ in range(nblk)]
-        self.ev_blk = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]
-                       for _ in range(nblk)]
+        # host path: the attention runs in head chunks, each chunk's output
+        # copied back (D2H stream) while the next chunk computes
+        self.out_chunks = max(1, min(H, int(os.environ.get("AC_STEADY_OUT_CHUNKS", "5"))))
+        self.d2h = torch.cuda.Stream()
+        self.chunk_done = [torch.cuda.Event() for _ in range(self.out_chunks)]
+        self.d2h_done = torch.cuda.Event()
+        # AC_STEADY_TRACE=1: timing events at phase boundaries (trace())
+        self.tracing = int(os.environ.get("AC_STEADY_TRACE", "0")) != 0
+        self.marks = []
+        self._keep = []
 
     # ------------------------------------------------------------------
+    def _mark(self, name: str):
+        if self.tracing:
+            e = torch.cuda.Event(enable_timing=True, external=True)
+            e.record()
+            self.marks.append((name, e))
+            self._keep.append(e)  # captured graphs reference it: never freed
+
+    def trace(self) -> list:
+        """(phase, ms since the step start) of the last replay (AC_STEADY_TRACE=1)."""
+        self.ev[2].synchronize()
+        torch.cuda.synchronize()
+        t0 = self.ev[0]
+        return [(n, round(t0.elapsed_time(e), 3)) for n, e in self.marks]
+
     def _enqueue(self, host=None):
+        self.marks = []
         """Every kernel of one warm step.  Heads are independent and the key
         side (Lloyd, envelopes, K/V permutation) and query side (normalise,
         Lloyd, reps) only meet at selection, so the clustering runs as
@@ -189,15 +203,17 @@ class SteadyStep:
         L.call("ac_l2norm_ex", self.Q.data_ptr(), self.dt, H * Ln, D, self.qn.data_ptr(),
                qb.xx.data_ptr(), self.qdeg.data_ptr(),
                qb.planes.data_ptr() if qb.planes is not None else 0, Ln, s)
+        self._mark("q_in+l2norm")
         self.fork.record(main)
         for i, (h0, h1) in enumerate(blocks):
             qs = self.streams[2 * i + 1]
             qs.wait_event(self.fork)
             with torch.cuda.stream(qs):
                 qb.lloyd_range(h0, h1, p.max_iter, p.tol, inertia=False, prepared=True)
-                self.joins[2 * i + 1].record(qs)
+                self._mark(f"qchain{i}")
         if host is not None:
             self.K.copy_(host[1], non_blocking=True)
+            self._mark("k_in")
             self.fork_k.record(main)
         else:
             self.fork_k = self.fork
@@ -206,63 +222,75 @@ class SteadyStep:
             ks.wait_event(self.fork_k)
             with torch.cuda.stream(ks):
                 kb.lloyd_range(h0, h1, p.max_iter, p.tol, inertia=False)
-                self.joins[2 * i].record(ks)
+                self._mark(f"kchain{i}")
         if host is not None:
             self.V.copy_(host[2], non_blocking=True)
-        if self.pipe:
+            self._mark("v_in")
             self.fork_v.record(main)
-            for i, (h0, h1) in enumerate(blocks):
-                ks = self.streams[2 * i]
-                ks.wait_event(self.joins[2 * i + 1])
-                ks.wait_event(self.fork_v)
-                with torch.cuda.stream(ks):
-                    self._tail(h0, h1, self.ev_blk[i])
-                    self.tails[i].record(ks)
-            for i in range(len(blocks)):
-                main.wait_event(self.tails[i])
-            self.ev[1].record()
-            self.ev[2].record()
         else:
-            for i in range(2 * len(blocks)):
-                main.wait_event(self.joins[i])
-            self._tail(0, H, self.ev[1:3])
-        if host is not None:
-            host[3].copy_(self.out, non_blocking=True)
-
-    def _tail(self, h0: int, h1: int, evs):
-        """Selection, layouts and attention of heads [h0, h1) on the current
-        stream (descriptor arrays and buffers offset to the head range)."""
-        Ln, D = self.L, self.D
-        nb = h1 - h0
-        kb = self.kb
-        s = L.stream_ptr()
-        psz = 8
+            self.fork_v = self.fork
         esz = self.K.element_size()
-        L.call("ac_segment_mean", self.reps_desc.data_ptr() + h0 * L.PROBLEM_DTYPE.itemsize, nb,
-               L.DTYPE_F32, D, self.gq, self.reps_ptrs.data_ptr() + h0 * psz, s)
-        L.call("ac_envelopes", self.env_desc.data_ptr() + h0 * L.PROBLEM_DTYPE.itemsize, nb, self.dt, D,
-               kb.max_k, self.pmax.data_ptr() + h0 * psz, self.pmin.data_ptr() + h0 * psz, s)
-        L.call("ac_select", self.sel_desc.data_ptr() + h0 * L.SELECT_DTYPE.itemsize, nb, D, self.scorer,
-               self.gq, kb.max_k, self.stride, s)
-        hoff = h0 * Ln * D * esz
-        L.call("ac_permute_rows_heads", self.K.data_ptr() + hoff, self.dt, D, self.kperm[h0].data_ptr(),
-               Ln, nb, self.kp.data_ptr() + hoff, s)
-        L.call("ac_permute_rows_heads", self.V.data_ptr() + hoff, self.dt, D, self.kperm[h0].data_ptr(),
-               Ln, nb, self.vp.data_ptr() + hoff, s)
-        qp = self.qp[h0 * self.qp_cap:]
-        qidx = self.qidx[h0 * (self.qp_cap + self.gq):]
-        items = self.items[h0 * self.item_cap * L.ITEM_DTYPE.itemsize:]
-        L.call("ac_build_q_layout", self.Q.data_ptr() + hoff, self.dt, D, Ln, nb, self.qperm[h0].data_ptr(),
-               self.qstarts[h0].data_ptr(), self.qcounts[h0].data_ptr(), self.qlab[h0].data_ptr(),
-               self.gq_t[h0:].data_ptr(), self.gq, self.nruns[h0].data_ptr(), self.stride,
-               qp.data_ptr(), qidx.data_ptr(), self.qp_cap, items.data_ptr(),
+        for i, (h0, h1) in enumerate(blocks):
+            # per-block tails of each chain: query reps / key envelopes and
+            # the K/V permutation (V after its copy) on the chain's stream
+            qs, ks = self.streams[2 * i + 1], self.streams[2 * i]
+            with torch.cuda.stream(qs):
+                L.call("ac_segment_mean", self.reps_desc.data_ptr() + h0 * L.PROBLEM_DTYPE.itemsize,
+                       h1 - h0, L.DTYPE_F32, D, self.gq, self.reps_ptrs.data_ptr() + h0 * 8,
+                       L.stream_ptr())
+                self.joins[2 * i + 1].record(qs)
+            with torch.cuda.stream(ks):
+                s = L.stream_ptr()
+                hoff = h0 * Ln * D * esz
+                L.call("ac_envelopes", self.env_desc.data_ptr() + h0 * L.PROBLEM_DTYPE.itemsize, h1 - h0,
+                       self.dt, D, kb.max_k, self.pmax.data_ptr() + h0 * 8, self.pmin.data_ptr() + h0 * 8, s)
+                L.call("ac_permute_rows_heads", self.K.data_ptr() + hoff, self.dt, D,
+                       self.kperm[h0].data_ptr(), Ln, h1 - h0, self.kp.data_ptr() + hoff, s)
+                ks.wait_event(self.fork_v)
+                L.call("ac_permute_rows_heads", self.V.data_ptr() + hoff, self.dt, D,
+                       self.kperm[h0].data_ptr(), Ln, h1 - h0, self.vp.data_ptr() + hoff, s)
+                self.joins[2 * i].record(ks)
+        for i in range(2 * len(blocks)):
+            main.wait_event(self.joins[i])
+        s = L.stream_ptr()
+        L.call("ac_select", self.sel_desc.data_ptr(), H, D, self.scorer, self.gq, kb.max_k,
+               self.stride, s)
+        L.call("ac_build_q_layout", self.Q.data_ptr(), self.dt, D, Ln, H, self.qperm.data_ptr(),
+               self.qstarts.data_ptr(), self.qcounts.data_ptr(), self.qlab.data_ptr(),
+               self.gq_t.data_ptr(), self.gq, self.nruns.data_ptr(), self.stride,
+               self.qp.data_ptr(), self.qidx.data_ptr(), self.qp_cap, self.items.data_ptr(),
                self.item_cap, self.item_rows, s)
-        evs[0].record()
-        L.call("ac_sparse_attention", qp.data_ptr(), nb * self.qp_cap, qidx.data_ptr(),
-               self.kp.data_ptr() + hoff, self.vp.data_ptr() + hoff, self.dt, D, Ln, nb, items.data_ptr(),
-               nb * self.item_cap, self.runs[h0].data_ptr(), self.scale,
-               self.out[h0].data_ptr(), self.odt, s)
-        evs[1].record()
+        self._mark("select+layout")
+        self.ev[1].record()
+        if host is None:
+            self._attend(0, H)
+        else:
+            nc = self.out_chunks
+            bounds = [(H * c) // nc for c in range(nc + 1)]
+            for c in range(nc):
+                h0, h1 = bounds[c], bounds[c + 1]
+                if h1 <= h0:
+                    continue
+                self._attend(h0, h1)
+                self.chunk_done[c].record(main)
+                self.d2h.wait_event(self.chunk_done[c])
+                with torch.cuda.stream(self.d2h):
+                    host[3][h0:h1].copy_(self.out[h0:h1], non_blocking=True)
+        self.ev[2].record()
+        self._mark("attention")
+        if host is not None:
+            self.d2h_done.record(self.d2h)
+            main.wait_event(self.d2h_done)
+            self._mark("out")
+
+    def _attend(self, h0: int, h1: int):
+        """Attention of the work items of heads [h0, h1) (layout built for all
+        heads: items carry absolute head indices), current stream."""
+        isz = L.ITEM_DTYPE.itemsize
+        L.call("ac_sparse_attention", self.qp.data_ptr(), self.H * self.qp_cap, self.qidx.data_ptr(),
+               self.kp.data_ptr(), self.vp.data_ptr(), self.dt, self.D, self.L, self.H,
+               self.items.data_ptr() + h0 * self.item_cap * isz, (h1 - h0) * self.item_cap,
+               self.runs.data_ptr(), self.scale, self.out.data_ptr(), self.odt, L.stream_ptr())
 
     def _capture(self, host=None):
         # one eager run on a side stream (lazy kernel attributes, workspaces),
@@ -312,12 +340,6 @@ class SteadyStep:
     def last_times_ms(self) -> dict:
         """Device time of the last step's phases (synchronises)."""
         self.ev[2].synchronize()
-        if self.pipe:
-            # per-block attention launches overlap later blocks' clustering:
-            # report their summed device time (on the launching streams)
-            att = sum(a.elapsed_time(b) for a, b in self.ev_blk)
-            return {"cluster_select_layout": self.ev[0].elapsed_time(self.ev[1]) - att,
-                    "attention": att}
         return {"cluster_select_layout": self.ev[0].elapsed_time(self.ev[1]),
                 "attention": self.ev[1].elapsed_time(self.ev[2])}
 
