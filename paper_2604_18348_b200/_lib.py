@@ -23,6 +23,7 @@ DTYPE_F32, DTYPE_BF16 = 0, 1
 ORDER_SEQ, ORDER_LANES16, ORDER_GEMV8 = 0, 1, 2
 SCORERS = {"quest": 0, "mean": 1, "clamped": 2, "given": 3}
 ASSIGN_MERGE, ASSIGN_ALL = 1, 2
+ASSIGN_LABELS_ONLY = 4
 ST_ACTIVE, ST_NITER, ST_DONE, ST_FLAGS, ST_KPP_STOP, ST_REPAIRS, ST_FIXUPS, ST_WIDE = range(8)
 ASSIGN_MODE_AUTO, ASSIGN_MODE_EXACT, ASSIGN_MODE_TC = range(3)
 LLOYD_NO_INERTIA = 1

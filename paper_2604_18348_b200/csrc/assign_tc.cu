@@ -39,6 +39,7 @@
 #include <climits>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "tc_common.cuh"
@@ -51,8 +52,9 @@ constexpr int BM = 128;     // rows per tile (== kAsgBM: shared tiling with the 
 constexpr int NBMAX = 128;  // centres per problem per launch (k - c_lo)
 constexpr int ATOM = BM * 128;  // one SW128 K-atom (64 bf16 columns) of a 128-row tile
 constexpr int MAXP = 32;    // problems per launch (tensor maps travel as kernel params)
-constexpr int THREADS = 320;
 constexpr int W_TMA = 0, W_MMA = 1, W_EPI0 = 2;
+constexpr int NWG_MAX = 3;  // epilogue warpgroups (one tile / TMEM accumulator each)
+constexpr int threads_for(int nwg) { return 64 + 128 * nwg; }
 constexpr int CF_STRIDE = 64 + 4;       // f32 centre rows (D = 64), padded against bank conflicts
 constexpr int QCAP = 64;                // per-warp queue of extra (row, centre) fix-up candidates
 constexpr int SMEM_MAX = 227 * 1024;
@@ -98,8 +100,8 @@ __host__ __device__ inline Layout make_layout(int dtype, int dim, int cap, int x
   l.off_cf = l.off_ab + cap * 32;
   l.off_cc = l.off_cf + (dim == 64 ? cap * CF_STRIDE * 4 : 0);
   l.off_hist = l.off_cc + NBMAX * 4;
-  l.off_q = l.off_hist + 2 * NBMAX * 4;
-  l.off_bar = l.off_q + 8 * QCAP * 8;
+  l.off_q = l.off_hist + NWG_MAX * NBMAX * 4;
+  l.off_bar = l.off_q + 4 * NWG_MAX * QCAP * 8;
   l.off_misc = l.off_bar + 16 * 8;
   l.smem = l.off_misc + 64 + 1024;  // + alignment slack
   return l;
@@ -198,9 +200,12 @@ AC_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 
-template <int DIM>
-__global__ void __launch_bounds__(THREADS, 1)
+// NWG = 2: 320 threads (<= 168 registers); NWG = 3: 448 threads, compiled
+// for 512 (<= 128 registers: 4 warps share an SM sub-partition's 64 KB file)
+template <int DIM, int NWG>
+__global__ void __launch_bounds__(NWG == 2 ? 320 : 512, 1)
 k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __restrict__ probs) {
+  constexpr int THREADS = threads_for(NWG);
   constexpr int KB = DIM / 64;           // SW128 K-atoms per row
   constexpr int PL_BYTES = KB * ATOM;    // one bf16 plane of a tile
   extern __shared__ __align__(1024) unsigned char smraw[];
@@ -213,8 +218,8 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + lay.off_bar);
   uint64_t* xfull = bars;        // [4] TMA -> MMA
   uint64_t* xempty = bars + 4;   // [4] epilogue -> TMA
-  uint64_t* afull = bars + 8;    // [2] MMA commit -> epilogue
-  uint64_t* aempty = bars + 10;  // [2] epilogue -> MMA
+  uint64_t* afull = bars + 8;          // [NWG] MMA commit -> epilogue
+  uint64_t* aempty = bars + 8 + NWG;   // [NWG] epilogue -> MMA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + lay.off_misc);
   int* s_ccmax = reinterpret_cast<int*>(sm + lay.off_misc + 16);
   float* s_cc = reinterpret_cast<float*>(sm + lay.off_cc);
@@ -229,7 +234,7 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       mbar_init(xfull + s, 1);
       mbar_init(xempty + s, 128);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NWG; ++b) {
       mbar_init(afull + b, 1);
       mbar_init(aempty + b, 128);
     }
@@ -242,7 +247,7 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
     if (j == 0) w = make_uint4(0x3f803f80u, 0x00003f80u, 0u, 0u);  // bf16 1.0 = 0x3f80
     *reinterpret_cast<uint4*>(aug_a + sw32(r, j)) = w;
   }
-  if (warp == W_MMA) tmem_alloc(tmem_slot, 256);
+  if (warp == W_MMA) tmem_alloc(tmem_slot, NWG == 2 ? 256 : 512);
   fence_proxy_async();
   fence_before();
   __syncthreads();
@@ -352,9 +357,9 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const int ci[6] = {0, 1, 2, 0, 1, 0};
         const int nterm = f32in ? 6 : 3;
         for (int i = 0; i < T; ++i) {
-          const int g = g0 + i, s = g % XS, b = g & 1;
+          const int g = g0 + i, s = g % XS, b = g % NWG;
           mbar_wait_sleep(xfull + s, (g / XS) & 1, 22);
-          if (g >= 2) mbar_wait_sleep(aempty + b, ((g >> 1) - 1) & 1, 23);
+          if (g >= NWG) mbar_wait_sleep(aempty + b, ((g / NWG) - 1) & 1, 23);
           fence_after();
           const uint32_t xa = smem_u32(sm + s * SB);
           const uint32_t d = tmem + (uint32_t)(b * 128);
@@ -395,19 +400,18 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const int64_t rw = (int64_t)(t + i - ptile0) * BM + r;
         return (i < T && rw < n) ? P.xx[rw] : 0.f;
       };
-      const int i_first = ((g0 & 1) == wg) ? 0 : 1;
+      const int i_first = (wg - g0 % NWG + NWG) % NWG;
       float xx_next = load_xx(i_first);
-      for (int i = 0; i < T; ++i) {
+      for (int i = i_first; i < T; i += NWG) {
         const int g = g0 + i;
-        if ((g & 1) != wg) continue;
         const int b = wg, s = g % XS;
         const int tile = t + i - ptile0;
         const int64_t row = (int64_t)tile * BM + r;
         const bool valid = row < n;
         const float xx = xx_next;
-        xx_next = load_xx(i + 2);
+        xx_next = load_xx(i + NWG);
         const float tb = 0x1p-15f * sqrtf(xx) * cmax + 0x1p-17f * (xx + ccmax) + 1e-30f;
-        mbar_wait_sleep(afull + b, (g >> 1) & 1, 26);
+        mbar_wait_sleep(afull + b, (g / NWG) & 1, 26);
         fence_after();
         const uint32_t acc_col = tmem + lane_base + (uint32_t)(b * 128);
         float m4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
@@ -549,7 +553,7 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
   __syncthreads();
   if (warp == W_MMA) {
     fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, NWG == 2 ? 256 : 512);
   }
 }
 
@@ -598,7 +602,8 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    for (const void* f : {(const void*)k_assign_tc<64>, (const void*)k_assign_tc<128>}) {
+    for (const void* f : {(const void*)k_assign_tc<64, 2>, (const void*)k_assign_tc<128, 2>,
+                          (const void*)k_assign_tc<64, 3>, (const void*)k_assign_tc<128, 3>}) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
       if (e != cudaSuccess) return check_cuda(e, "k_assign_tc smem");
     }
@@ -634,10 +639,17 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     const int total = prm.tile0[np];
     if (total == 0) continue;
     const int grid = std::min(total, sms);
-    if (d == 64)
-      k_assign_tc<64><<<grid, THREADS, prm.lay.smem, st>>>(prm, probs + p0);
-    else
-      k_assign_tc<128><<<grid, THREADS, prm.lay.smem, st>>>(prm, probs + p0);
+    // bf16 points: 3 epilogue warpgroups (4 x-stages still leave one in
+    // flight); f32 points: their 48 KB stages allow only 3, so 2 warpgroups
+    static const int env_wg = getenv("AC_ASG_WG") ? atoi(getenv("AC_ASG_WG")) : 0;
+    const int nwg = env_wg ? env_wg : (dtype == AC_DTYPE_BF16 ? 3 : 2);
+    if (nwg == 2) {
+      if (d == 64) k_assign_tc<64, 2><<<grid, threads_for(2), prm.lay.smem, st>>>(prm, probs + p0);
+      else k_assign_tc<128, 2><<<grid, threads_for(2), prm.lay.smem, st>>>(prm, probs + p0);
+    } else {
+      if (d == 64) k_assign_tc<64, 3><<<grid, threads_for(3), prm.lay.smem, st>>>(prm, probs + p0);
+      else k_assign_tc<128, 3><<<grid, threads_for(3), prm.lay.smem, st>>>(prm, probs + p0);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return check_cuda(e, "k_assign_tc");
   }
