@@ -95,6 +95,7 @@ _SIGS = {
     "ac_sparse_attention": [_P, _I64, _P, _P, _P, _I, _I, _I64, _I, _P, _I, _P, _F, _P, _I, _P],
     "ac_sparse_attention_fa4": [_P, _I64, _P, _P, _P, _I, _I64, _I, _P, _I, _P, _F, _P, _I, _P],
     "ac_sparse_attention_tc": [_P, _I64, _P, _P, _P, _I, _I64, _I, _P, _I, _P, _F, _P, _I, _P],
+    "ac_sparse_attention_fa4_d128": [_P, _I64, _P, _P, _P, _I, _I64, _I, _P, _I, _P, _F, _P, _I, _P],
     "ac_sparse_attention_simt": [_P, _P, _P, _P, _I, _I, _I64, _P, _I, _P, _F, _P, _I, _P],
 }
 _RESTYPES = {"ac_last_error": ctypes.c_char_p, "ac_pw_plan_len": _I64}

@@ -35,6 +35,7 @@ UNITS = {
     "attn_simt.cu": [],
     "attn_tc.cu": [],
     "attn_fa4.cu": [],
+    "attn_fa4_d128.cu": [],
     "assign_tc.cu": ["--fmad=false"],
 }
 

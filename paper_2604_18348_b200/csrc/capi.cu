@@ -179,7 +179,7 @@ extern "C" int ac_gemm_order(int64_t m, int64_t n, int64_t d) {
 // otherwise (f32 inputs need f32 numerics for the 1e-4 parity bar)
 // ---------------------------------------------------------------------------
 extern "C" int ac_attention_item_rows(int dtype, int d) {
-  return (dtype == AC_DTYPE_BF16 && d == 64) ? 256 : 128;
+  return (dtype == AC_DTYPE_BF16 && (d == 64 || d == 128)) ? 256 : 128;
 }
 
 extern "C" int ac_sparse_attention(const void* q, int64_t q_rows_total, const int32_t* qidx,
@@ -191,7 +191,7 @@ extern "C" int ac_sparse_attention(const void* q, int64_t q_rows_total, const in
     return ac_sparse_attention_fa4(q, q_rows_total, qidx, k, v, d, L, heads, items, nitems, runs,
                                    scale, out, out_dtype, stream);
   if (dtype == AC_DTYPE_BF16 && d == 128)
-    return ac_sparse_attention_tc(q, q_rows_total, qidx, k, v, d, L, heads, items, nitems, runs,
+    return ac_sparse_attention_fa4_d128(q, q_rows_total, qidx, k, v, d, L, heads, items, nitems, runs,
                                   scale, out, out_dtype, stream);
   return ac_sparse_attention_simt(q, qidx, k, v, dtype, d, L, items, nitems, runs, scale, out,
                                   out_dtype, stream);

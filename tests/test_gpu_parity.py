@@ -239,10 +239,11 @@ def test_dense_attention_tcgen05_bf16(gpu, oracle, H, L, D):
         assert rel_l2(ref, out[h]) <= BF16_TOL
 
 
-def test_sparse_tcgen05_matches_simt(gpu):
+@pytest.mark.parametrize("D", [64, 128])
+def test_sparse_tcgen05_matches_simt(gpu, D):
     """Same runs/items through both attention kernels (bf16 inputs)."""
     from paper_2604_18348_b200.pipeline import LayerRunner
-    q, k, v = gen_synthetic(CRIT7_SPEC, 6000, 64, 2, 1, 3)[0][0]
+    q, k, v = gen_synthetic(CRIT7_SPEC, 6000, D, 2, 1, 3)[0][0]
     Q, K, V = (torch.stack([torch.from_numpy(a)] * 2).bfloat16().cuda().contiguous()
                for a in (q, k, v))
     p = gpu.PipelineParams(q_clusters=65, topk=25, full_layer_quota=0.0)
