@@ -1529,6 +1529,98 @@ __global__ void k_envelopes(const ac_cluster_problem* __restrict__ probs, int dt
   }
 }
 
+// D = 32*DPL fast path: one CTA per cluster, its 8 warps scanning 8
+// contiguous chunks of the member list (lane = DPL dimensions, 8 member rows
+// in flight), then the chunk results combined in chunk order.  The sequential
+// fold keeps the first maximal element (ties such as +0/-0 keep the earlier
+// one, the first NaN wins); folding chunk results in order with the same
+// np.maximum / np.minimum gives exactly the same element.
+constexpr int kEnvWarps = 8;
+
+template <int DPL, bool BF16>
+__global__ void __launch_bounds__(32 * kEnvWarps)
+k_envelopes_w(const ac_cluster_problem* __restrict__ probs, float* const* env_max,
+              float* const* env_min) {
+  constexpr int D = 32 * DPL;
+  __shared__ float s_mx[kEnvWarps][D], s_mn[kEnvWarps][D];
+  __shared__ int s_has[kEnvWarps];
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  const int c = blockIdx.x;
+  if (c >= P.k) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cnt = P.counts[c], s0 = P.starts[c];
+  const int per = (cnt + kEnvWarps - 1) / kEnvWarps;
+  const int m0 = min(cnt, warp * per), m1 = min(cnt, m0 + per);
+  const int32_t* perm = P.perm + s0;
+  float a[DPL], b[DPL];
+  auto load_row = [&](int32_t row, float (&v)[DPL]) {
+    if constexpr (BF16) {
+      const __nv_bfloat16* xr = reinterpret_cast<const __nv_bfloat16*>(P.x) + (int64_t)row * D + lane * DPL;
+      if constexpr (DPL == 2) {
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(xr));
+        v[0] = __uint_as_float(w << 16); v[1] = __uint_as_float(w & 0xffff0000u);
+      } else {
+        const uint2 w = __ldg(reinterpret_cast<const uint2*>(xr));
+        v[0] = __uint_as_float(w.x << 16); v[1] = __uint_as_float(w.x & 0xffff0000u);
+        v[2] = __uint_as_float(w.y << 16); v[3] = __uint_as_float(w.y & 0xffff0000u);
+      }
+    } else {
+      const float* xr = reinterpret_cast<const float*>(P.x) + (int64_t)row * D + lane * DPL;
+      if constexpr (DPL == 2) {
+        const float2 f = __ldg(reinterpret_cast<const float2*>(xr));
+        v[0] = f.x; v[1] = f.y;
+      } else {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(xr));
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+      }
+    }
+  };
+  if (m0 < m1) {
+    float v[DPL];
+    load_row(perm[m0], v);
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) { a[i] = v[i]; b[i] = v[i]; }
+    int m = m0 + 1;
+    for (; m + 8 <= m1; m += 8) {
+      int32_t rows[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) rows[u] = perm[m + u];
+      float w[8][DPL];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) load_row(rows[u], w[u]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) { a[i] = np_maximum(a[i], w[u][i]); b[i] = np_minimum(b[i], w[u][i]); }
+    }
+    for (; m < m1; ++m) {
+      load_row(perm[m], v);
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) { a[i] = np_maximum(a[i], v[i]); b[i] = np_minimum(b[i], v[i]); }
+    }
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      s_mx[warp][lane * DPL + i] = a[i];
+      s_mn[warp][lane * DPL + i] = b[i];
+    }
+  }
+  if (lane == 0) s_has[warp] = m0 < m1;
+  __syncthreads();
+  float* mx = env_max[blockIdx.y] + (int64_t)c * D;
+  float* mn = env_min[blockIdx.y] + (int64_t)c * D;
+  for (int t = threadIdx.x; t < D; t += blockDim.x) {
+    float x = 0.f, y = 0.f;  // empty cluster: zeros, as the sequential kernel
+    bool any = false;
+    for (int w = 0; w < kEnvWarps; ++w) {
+      if (!s_has[w]) continue;
+      if (!any) { x = s_mx[w][t]; y = s_mn[w][t]; any = true; }
+      else { x = np_maximum(x, s_mx[w][t]); y = np_minimum(y, s_mn[w][t]); }
+    }
+    mx[t] = x;
+    mn[t] = y;
+  }
+}
+
 }  // namespace ac
 
 // ===========================================================================
@@ -1963,7 +2055,19 @@ extern "C" int ac_envelopes(const ac_cluster_problem* probs, int nprob, int dtyp
                             int max_k, float* const* env_max, float* const* env_min,
                             void* stream) {
   if (nprob <= 0) return AC_OK;
-  k_envelopes<<<dim3((max_k + 7) / 8, nprob), 256, 0, S(stream)>>>(probs, dtype, d, env_max, env_min);
+  if ((d == 64 || d == 128) && (dtype == AC_DTYPE_BF16 || dtype == AC_DTYPE_F32)) {
+    const dim3 grid((unsigned)max_k, nprob);
+    const bool bf = dtype == AC_DTYPE_BF16;
+    if (d == 64) {
+      if (bf) k_envelopes_w<2, true><<<grid, 32 * kEnvWarps, 0, S(stream)>>>(probs, env_max, env_min);
+      else k_envelopes_w<2, false><<<grid, 32 * kEnvWarps, 0, S(stream)>>>(probs, env_max, env_min);
+    } else {
+      if (bf) k_envelopes_w<4, true><<<grid, 32 * kEnvWarps, 0, S(stream)>>>(probs, env_max, env_min);
+      else k_envelopes_w<4, false><<<grid, 32 * kEnvWarps, 0, S(stream)>>>(probs, env_max, env_min);
+    }
+  } else {
+    k_envelopes<<<dim3((max_k + 7) / 8, nprob), 256, 0, S(stream)>>>(probs, dtype, d, env_max, env_min);
+  }
   AC_CHECK_LAUNCH("k_envelopes");
   return AC_OK;
 }

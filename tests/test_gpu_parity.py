@@ -254,3 +254,21 @@ def test_sparse_tcgen05_matches_simt(gpu, D):
         so = run.sparse(Q, K, V, plan.q_models, plan.reps, plan.key_models, 25)
         outs[impl] = so.out.cpu().numpy()
     assert rel_l2(outs["simt"], outs["auto"]) <= BF16_TOL
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_envelopes_large_clusters_signed_zeros(gpu, oracle, d):
+    """k_envelopes_w (8 warps per cluster, chunk results folded in order) vs
+    the sequential np.maximum/np.minimum fold, with +0/-0 ties and large
+    clusters so that every warp has a chunk."""
+    rng = np.random.default_rng(d)
+    x = rng.normal(size=(6000, d)).astype(np.float32)
+    x[:, 0] = np.where(rng.random(6000) < 0.5, 0.0, -0.0).astype(np.float32)
+    x[:, 1] = np.abs(x[:, 1]) * -1.0
+    x[::3, 1] = -0.0
+    x[::5, 1] = 0.0
+    m = oracle.kmeans(x, 7, 2)
+    env_o = oracle.envelopes(x, m)
+    env_g = gpu.build_envelopes(x, m)
+    assert np.array_equal(env_g.max_vec.view(np.int32), env_o.max_vec.view(np.int32))
+    assert np.array_equal(env_g.min_vec.view(np.int32), env_o.min_vec.view(np.int32))
