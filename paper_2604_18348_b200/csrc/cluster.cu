@@ -890,15 +890,15 @@ k_update_w(const ac_cluster_problem* __restrict__ probs, int d, double tol, int 
   const int k = P.k;
   if (c >= k) return;
   constexpr int ESZ = BF16 ? 2 : 4;
-  const int row_bytes = d * ESZ;
-  const int stage_bytes = kUpdWRows * row_bytes;
+  constexpr int row_bytes = 32 * DPL * ESZ;  // d == 32 * DPL (host dispatch)
+  constexpr int stage_bytes = kUpdWRows * row_bytes;
   unsigned char* ring = wsm + (size_t)warp * kUpdWStages * stage_bytes;
   float* s_sq = reinterpret_cast<float*>(wsm + (size_t)kUpdWarps * kUpdWStages * stage_bytes) +
                 warp * 2 * d;
   const int cnt = P.counts[c], s0 = P.starts[c];
   const int32_t* perm = P.perm + s0;
   const char* xb = reinterpret_cast<const char*>(P.x);
-  const int cpr = row_bytes / 16;        // 16-byte pieces per row
+  constexpr int cpr = row_bytes / 16;    // 16-byte pieces per row
   const int nb = (cnt + kUpdWRows - 1) / kUpdWRows;
 
   // member indices are register-prefetched one stage ahead of their rows
@@ -1042,6 +1042,7 @@ k_update_w(const ac_cluster_problem* __restrict__ probs, int d, double tol, int 
 // ---------------------------------------------------------------------------
 constexpr int kUsChunk = 128;  // members per warp task
 constexpr int kUsWarps = 8;
+constexpr int kUsGroup = 8;    // member rows in flight per warp (16 measured slower)
 
 // lane's DPL consecutive dimensions of row `row` (one vector load)
 template <int DPL, bool BF16>
@@ -1108,16 +1109,16 @@ k_usum(const ac_cluster_problem* __restrict__ probs, int d) {
   for (int j = 0; j < m1; j += 32) {
     const int pj = pj_next;  // member indices of this 32-member group (prefetched)
     pj_next = (j + 32 + lane < m1) ? P.perm[m0 + j + 32 + lane] : 0;
-    for (int g = 0; g < 32; g += 8) {
+    for (int g = 0; g < 32; g += kUsGroup) {
       if (j + g >= m1) break;
-      float v[8][DPL];
+      float v[kUsGroup][DPL];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
+      for (int r = 0; r < kUsGroup; ++r) {
         const int row = __shfl_sync(0xffffffffu, pj, g + r);
         if (j + g + r < m1) load_row_part<DPL, BF16>(P.x, row, d, lane, v[r]);
       }
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
+      for (int r = 0; r < kUsGroup; ++r) {
         const int64_t m = m0 + j + g + r;
         if (j + g + r >= m1) break;
         while (m >= c_end) {  // cluster boundary (warp-uniform)
