@@ -174,10 +174,13 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
       mbar_init(kv_empty + s, 1);
     }
     for (int t = 0; t < 2; ++t) {
+      // only warps holding at least one real query row take part (the rest
+      // of a partial tile's rows are padding and skip the softmax entirely)
+      const int live = 32 * max(1, min(4, (min(BM, it.q_rows - t * BM) + 31) / 32));
       mbar_init(s_full + t, 1);
-      mbar_init(p_full + t, 128);
+      mbar_init(p_full + t, live);
       mbar_init(o_done + t, 1);
-      mbar_init(s_free + t, 128);
+      mbar_init(s_free + t, live);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -280,7 +283,8 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
     const uint32_t tP = tmem + lane_base + COL_P + t * 64;
     float m_run = -INFINITY, l_run = 0.f;
     int j = 0;
-    if (t == 0 || two) {
+    const bool live = q4 * 32 < it.q_rows - t * BM;  // this warp holds real rows
+    if ((t == 0 || two) && live) {
       TileIter ti(iruns, it.nruns);
       int start, nk;
       while (ti.next(start, nk)) {

@@ -134,8 +134,10 @@ k_attn_fa4_d128(const __grid_constant__ CUtensorMap tmq, const __grid_constant__
       mbar_init(kv_empty + s, 1);
     }
     for (int t = 0; t < 2; ++t) {
+      // only warps holding at least one real query row take part
+      const int live = 32 * max(1, min(4, (min(BM, it.q_rows - t * BM) + 31) / 32));
       mbar_init(s_full + t, 1);
-      mbar_init(p_full + t, 128);
+      mbar_init(p_full + t, live);
       mbar_init(o_done + t, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -251,7 +253,8 @@ k_attn_fa4_d128(const __grid_constant__ CUtensorMap tmq, const __grid_constant__
     const uint32_t tO = tmem + lane_base + COL_O + t * D;
     float m_run = -INFINITY, l_run = 0.f;
     int j = 0;
-    if (t < ntile) {
+    const bool live = q4 * 32 < it.q_rows - t * BM;  // this warp holds real rows
+    if (t < ntile && live) {
       TileIter ti(iruns, it.nruns);
       int start, nk;
       while (ti.next(start, nk)) {
@@ -294,6 +297,12 @@ k_attn_fa4_d128(const __grid_constant__ CUtensorMap tmq, const __grid_constant__
         uint64_t acc0 = pk2(0.f, 0.f), acc1 = pk2(0.f, 0.f);
 #pragma unroll
         for (int ch = 0; ch < BN / 32; ++ch) {
+          if (ch * 32 >= nk) {  // whole chunk past the run's end: P = 0, no exponentials
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sr[ch][i] = 0u;
+            tmem_st16(tS + ch * 16, sr[ch]);
+            continue;
+          }
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const uint64_t x =
