@@ -166,3 +166,52 @@ def default_schedule(m0: int):
     def schedule(t, remaining, total):
         return m0 if t == 0 else max(STAGE_FLOOR, math.ceil(m0 * remaining / total))
     return schedule
+
+
+# ---------------------------------------------------------------------------
+# evaluation: per-layer compactness (clustering.py:323-362), on the device
+# ---------------------------------------------------------------------------
+@dataclass
+class CompactnessReport:
+    mse_per_head: list    # mean squared token-to-assigned-centre distance per head
+    mse_layer: float      # mean over heads
+    comp: float           # 1 / mse_layer (inf when exactly zero)
+    db_index: float       # Davies-Bouldin index, averaged over heads
+
+
+def _davies_bouldin(x: torch.Tensor, cen: torch.Tensor, lab: torch.Tensor, cnt: torch.Tensor) -> float:
+    """DB = mean_i max_{j != i} (S_i + S_j) / M_ij in f64 (clustering.py:323-337)."""
+    c = cen.shape[0]
+    if c < 2:
+        return 0.0
+    dist = torch.linalg.norm(x - cen[lab], dim=1)
+    s = torch.zeros(c, dtype=torch.float64, device=x.device).index_add_(0, lab, dist) / cnt
+    m = torch.cdist(cen, cen)
+    ratio = (s[:, None] + s[None, :]) / torch.where(m > 0, m, torch.full_like(m, math.inf))
+    ratio.fill_diagonal_(-math.inf)
+    return float(ratio.max(dim=1).values.mean().item())
+
+
+def compactness(k_heads, models) -> CompactnessReport:
+    """Per-layer compactness of per-head key clusterings: per-head MSE, the
+    layer's 1/MSE and the mean Davies-Bouldin index (clustering.py:340-362),
+    evaluated on the GPU in f64 (agrees with the reference to f64 rounding:
+    the reductions run in a different order)."""
+    if len(k_heads) != len(models):
+        raise ParameterError(f"{len(k_heads)} key tensors but {len(models)} models")
+    mse, db = [], []
+    for x, m in zip(k_heads, models):
+        xd, _ = to_device(x, keep_bf16=False)
+        xd = xd.double()
+        cen = torch.as_tensor(np.asarray(m.centers) if not isinstance(m.centers, torch.Tensor)
+                              else m.centers).to(xd.device).double()
+        lab = torch.as_tensor(np.asarray(m.assignments) if not isinstance(m.assignments, torch.Tensor)
+                              else m.assignments).to(xd.device).long()
+        cnt = torch.as_tensor(np.asarray(m.counts) if not isinstance(m.counts, torch.Tensor)
+                              else m.counts).to(xd.device).double()
+        mse.append(float(((xd - cen[lab]) ** 2).sum(dim=1).mean().item()))
+        db.append(_davies_bouldin(xd, cen, lab, cnt))
+    mse_layer = float(np.mean(mse))
+    return CompactnessReport(mse_per_head=mse, mse_layer=mse_layer,
+                             comp=math.inf if mse_layer == 0.0 else 1.0 / mse_layer,
+                             db_index=float(np.mean(db)))

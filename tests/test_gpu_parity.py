@@ -272,3 +272,24 @@ def test_envelopes_large_clusters_signed_zeros(gpu, oracle, d):
     env_g = gpu.build_envelopes(x, m)
     assert np.array_equal(env_g.max_vec.view(np.int32), env_o.max_vec.view(np.int32))
     assert np.array_equal(env_g.min_vec.view(np.int32), env_o.min_vec.view(np.int32))
+
+
+def test_compactness_matches_scalar_loops(gpu):
+    """GPU compactness (f64) vs the reference test's scalar loops
+    (tests/test_clustering.py:240-275 of the reference)."""
+    import math
+    rng = np.random.default_rng(18)
+    x = rng.normal(size=(60, 3)).astype(np.float32)
+    m = gpu.kmeans(x, 4, seed=3)
+    rep = gpu.compactness([x], [m])
+    mse = np.mean([np.linalg.norm(x[i].astype(np.float64) - m.centers[m.assignments[i]]) ** 2
+                   for i in range(60)])
+    assert rep.mse_layer == pytest.approx(mse, rel=1e-12)
+    s = [np.mean([np.linalg.norm(x[i].astype(np.float64) - m.centers[c]) for i in range(60)
+                  if m.assignments[i] == c]) for c in range(4)]
+    db = np.mean([max((s[i] + s[j]) / np.linalg.norm(m.centers[i].astype(np.float64) - m.centers[j])
+                      for j in range(4) if j != i) for i in range(4)])
+    assert rep.db_index == pytest.approx(db, rel=1e-12)
+    z = np.tile(np.array([[1.0, 1.0]], np.float32), (4, 1))
+    rz = gpu.compactness([z], [gpu.kmeans(z, 1, seed=0)])
+    assert rz.mse_layer == 0.0 and math.isinf(rz.comp)
