@@ -207,9 +207,12 @@ int ac_get_assign_mode(void);
 /* centroid-update kernel selection (process-wide): 0 = split-chain sums with
  * an exact f32 enclosure test (member-order chain per dimension only when
  * the enclosure straddles a rounding boundary) when the batch has csum/cabs
- * workspaces, 1 = always the member-order f64 chains.  Both are
- * bit-identical to np.add.reduceat in member order.                        */
+ * workspaces, 1 = always the member-order f64 chains (the default: its
+ * small per-centre grid co-runs with the other Lloyd chains of a step and
+ * measured faster end to end).  Both are bit-identical to np.add.reduceat
+ * in member order.  Env AC_UPDATE_MODE overrides the default at load.      */
 int ac_set_update_mode(int mode);
+int ac_get_update_mode(void);
 int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dtype,
                    int d, int64_t max_n, int max_k, int iter, int flags,
                    void* stream);

@@ -76,6 +76,7 @@ _SIGS = {
     "ac_set_assign_mode": [_I],
     "ac_get_assign_mode": [],
     "ac_set_update_mode": [_I],
+    "ac_get_update_mode": [],
     "ac_repair_sort": [_P, _I, _I, _I, _I64, _I, _I, _I, _P],
     "ac_segment_mean": [_P, _I, _I, _I, _I, _P, _P],
     "ac_sort_by_label": [_P, _I, _I64, _I, _P],

@@ -9,6 +9,7 @@
 // reference.  Compiled with --fmad=false.
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "pairwise.cuh"
@@ -1638,7 +1639,8 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
 
 namespace {
 int g_assign_mode = AC_ASSIGN_MODE_AUTO;
-int g_update_mode = 0;  // 0: split-chain update when eligible, 1: member-order chains
+// 0: split-chain update when eligible, 1: member-order chains (default)
+int g_update_mode = getenv("AC_UPDATE_MODE") ? atoi(getenv("AC_UPDATE_MODE")) : 1;
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int set_smem(const void* fn, size_t bytes) {
@@ -1820,6 +1822,8 @@ extern "C" int ac_set_update_mode(int mode) {
   g_update_mode = mode;
   return AC_OK;
 }
+
+extern "C" int ac_get_update_mode(void) { return g_update_mode; }
 
 static int repair_sort_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
                             int64_t max_n, int max_k, int iter, int flags, cudaStream_t st) {

@@ -141,12 +141,13 @@ def test_split_chain_update_matches_member_order(gpu, dtype, d, k):
     tdt = torch.float32 if dtype == "f32" else torch.bfloat16
     xs = [(torch.randn(12000 + 777 * h, d, generator=g) * (1 + h)).to(tdt).cuda() for h in range(3)]
     runs = []
+    prev = int(L.lib().ac_get_update_mode())
     for mode in (0, 1):
         L.call("ac_set_update_mode", mode)
         try:
             ms = E.kmeans_batch(xs, [k] * 3, [1, 2, 3], 25, 1e-4)
         finally:
-            L.call("ac_set_update_mode", 0)
+            L.call("ac_set_update_mode", prev)
         torch.cuda.synchronize()
         runs.append([(m.centers.clone(), m.labels.clone(), m.n_iter()) for m in ms])
     for (c0, l0, n0), (c1, l1, n1) in zip(*runs):
