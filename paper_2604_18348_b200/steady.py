@@ -147,8 +147,10 @@ class SteadyStep:
         nblk = (H + self.hb - 1) // self.hb
         self.streams = [torch.cuda.Stream() for _ in range(2 * nblk)]
         self.fork = torch.cuda.Event()
-        self.fork_k = torch.cuda.Event()
         self.fork_v = torch.cuda.Event()
+        self.h2d = torch.cuda.Stream()
+        self.q_in = [torch.cuda.Event() for _ in range(nblk)]
+        self.k_in = [torch.cuda.Event() for _ in range(nblk)]
         self.host_graphs = {}
         self.joins = [torch.cuda.Event() for _ in range(2 * nblk)]
         # host path: the attention runs in head chunks, each chunk's output
@@ -196,39 +198,43 @@ class SteadyStep:
         main = torch.cuda.current_stream()
         blocks = [(h0, min(H, h0 + self.hb)) for h0 in range(0, H, self.hb)]
         self.ev[0].record()
-        if host is not None:
-            self.Q.copy_(host[0], non_blocking=True)
-        s = L.stream_ptr()
-        # normalisation + the query Batch's prepare (xx, f32 planes) in one pass
-        L.call("ac_l2norm_ex", self.Q.data_ptr(), self.dt, H * Ln, D, self.qn.data_ptr(),
-               qb.xx.data_ptr(), self.qdeg.data_ptr(),
-               qb.planes.data_ptr() if qb.planes is not None else 0, Ln, s)
-        self._mark("q_in+l2norm")
         self.fork.record(main)
+        # host path: per-block H2D copies on their own stream in the order the
+        # chains need them (Q0 K0 Q1 K1 ... V), so block 0's clustering starts
+        # after 1/(2*nblk) of the input has arrived instead of all of Q
+        if host is not None:
+            self.h2d.wait_event(self.fork)
         for i, (h0, h1) in enumerate(blocks):
-            qs = self.streams[2 * i + 1]
-            qs.wait_event(self.fork)
+            qs, ks = self.streams[2 * i + 1], self.streams[2 * i]
+            if host is not None:
+                with torch.cuda.stream(self.h2d):
+                    self.Q[h0:h1].copy_(host[0][h0:h1], non_blocking=True)
+                    self.q_in[i].record(self.h2d)
+                    self.K[h0:h1].copy_(host[1][h0:h1], non_blocking=True)
+                    self.k_in[i].record(self.h2d)
+                qs.wait_event(self.q_in[i])
+                ks.wait_event(self.k_in[i])
+            else:
+                qs.wait_event(self.fork)
+                ks.wait_event(self.fork)
             with torch.cuda.stream(qs):
+                # normalisation + the query Batch's prepare (xx, f32 planes) in one pass
+                r0 = h0 * Ln
+                L.call("ac_l2norm_ex", self.Q[h0].data_ptr(), self.dt, (h1 - h0) * Ln, D,
+                       self.qn[h0].data_ptr(), qb.xx.data_ptr() + 4 * r0, self.qdeg.data_ptr() + r0,
+                       qb.planes.data_ptr() + 2 * 3 * r0 * D if qb.planes is not None else 0, Ln,
+                       L.stream_ptr())
                 qb.lloyd_range(h0, h1, p.max_iter, p.tol, inertia=False, prepared=True)
                 self._mark(f"qchain{i}")
-        if host is not None:
-            self.K.copy_(host[1], non_blocking=True)
-            self._mark("k_in")
-            self.fork_k.record(main)
-        else:
-            self.fork_k = self.fork
-        for i, (h0, h1) in enumerate(blocks):
-            ks = self.streams[2 * i]
-            ks.wait_event(self.fork_k)
             with torch.cuda.stream(ks):
                 kb.lloyd_range(h0, h1, p.max_iter, p.tol, inertia=False)
                 self._mark(f"kchain{i}")
         if host is not None:
-            self.V.copy_(host[2], non_blocking=True)
-            self._mark("v_in")
-            self.fork_v.record(main)
+            with torch.cuda.stream(self.h2d):
+                self.V.copy_(host[2], non_blocking=True)
+                self.fork_v.record(self.h2d)
         else:
-            self.fork_v = self.fork
+            self.fork_v.record(main)
         esz = self.K.element_size()
         for i, (h0, h1) in enumerate(blocks):
             # per-block tails of each chain: query reps / key envelopes and
