@@ -437,14 +437,16 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
           uint32_t v[16];
           tmem_ld16(acc_col + ch * 16, v);
           tmem_wait_ld();
-          uint32_t m = 0;
+          // four independent partial masks (short dependency chains)
+          uint32_t mq[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-          for (int u = 0; u < 16; ++u) m |= (__uint_as_float(v[u]) <= ethr) ? (1u << u) : 0u;
-          mk[ch >> 1] |= m << ((ch & 1) * 16);
-          if (m) {
-            c1 = min(c1, ch * 16 + __ffs(m) - 1);
-            ncand += __popc(m);
-          }
+          for (int u = 0; u < 16; ++u) mq[u & 3] |= (__uint_as_float(v[u]) <= ethr) ? (1u << u) : 0u;
+          mk[ch >> 1] |= ((mq[0] | mq[1]) | (mq[2] | mq[3])) << ((ch & 1) * 16);
+        }
+#pragma unroll
+        for (int w = NBMAX / 32 - 1; w >= 0; --w) {
+          if (mk[w]) c1 = w * 32 + __ffs(mk[w]) - 1;  // lowest set bit overall
+          ncand += __popc(mk[w]);
         }
         fence_before();
         mbar_arrive(aempty + b);
