@@ -82,6 +82,7 @@ struct Params {
   int dtype;
   int c_lo;
   int flags;
+  int f32_terms;  // split products for f32 points: 3 (default) or 6
   Layout lay;
 };
 
@@ -350,12 +351,15 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const uint32_t idesc = idesc_bf16(BM, nbp, false);
         const uint32_t ca = smem_u32(cplanes);
         const uint32_t aa = smem_u32(aug_a), ab = smem_u32(aug_b);
-        // plane products kept: (x plane, c plane), the x-hi terms first (bf16
-        // points are exact in plane 0, so they use only those three); the
-        // dropped terms are < 2^-23 relative
-        const int xi[6] = {0, 0, 0, 1, 1, 2};
-        const int ci[6] = {0, 1, 2, 0, 1, 0};
-        const int nterm = f32in ? 6 : 3;
+        // plane products kept, (x plane, c plane): bf16 points are exact in
+        // plane 0 -> x.c_hi, x.c_mid, x.c_lo (the exact product); f32 points
+        // -> the three largest, hi.hi, hi.mid, mid.hi (the dropped ones are
+        // < 3.02*2^-18 sum|x_i c'_i|, covered by the widened epilogue bound),
+        // or all six with AC_ASG_F32_TERMS=6 (dropped < 2^-26)
+        const bool six = f32in && prm.f32_terms == 6;
+        const int xi[6] = {0, 0, f32in ? 1 : 0, 0, 1, 2};
+        const int ci[6] = {0, 1, f32in ? 0 : 2, 2, 1, 0};
+        const int nterm = six ? 6 : 3;
         for (int i = 0; i < T; ++i) {
           const int g = g0 + i, s = g % XS, b = g % NWG;
           mbar_wait_sleep(xfull + s, (g / XS) & 1, 22);
@@ -410,7 +414,10 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         const bool valid = row < n;
         const float xx = xx_next;
         xx_next = load_xx(i + NWG);
-        const float tb = 0x1p-15f * sqrtf(xx) * cmax + 0x1p-17f * (xx + ccmax) + 1e-30f;
+        // |e~ - e_ref| <= tb for every column (assignment); with
+        // only three split products for f32 points, + 0x1.9p-16 ||x|| cmax
+        const float tb = (0x1p-15f + (f32in && prm.f32_terms != 6 ? 0x1.9p-16f : 0.f)) * sqrtf(xx) * cmax +
+                         0x1p-17f * (xx + ccmax) + 1e-30f;
         mbar_wait_sleep(afull + b, (g / NWG) & 1, 26);
         fence_after();
         const uint32_t acc_col = tmem + lane_base + (uint32_t)(b * 128);
@@ -626,6 +633,8 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     prm.dtype = dtype;
     prm.c_lo = c_lo;
     prm.flags = flags;
+    static const int f32_terms = getenv("AC_ASG_F32_TERMS") ? atoi(getenv("AC_ASG_F32_TERMS")) : 3;
+    prm.f32_terms = f32_terms == 6 ? 6 : 3;
     prm.tile0[0] = 0;
     for (int j = 0; j < np; ++j) {
       const ac_cluster_problem& P = host_probs[p0 + j];
