@@ -650,10 +650,10 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     const int total = prm.tile0[np];
     if (total == 0) continue;
     const int grid = std::min(total, sms);
-    // bf16 points: 3 epilogue warpgroups (4 x-stages still leave one in
-    // flight); f32 points: their 48 KB stages allow only 3, so 2 warpgroups
-    static const int env_wg = getenv("AC_ASG_WG") ? atoi(getenv("AC_ASG_WG")) : 0;
-    const int nwg = env_wg ? env_wg : (dtype == AC_DTYPE_BF16 ? 3 : 2);
+    // 3 epilogue warpgroups (measured faster than 2 for both dtypes once the
+    // f32 MMA runs three split products); AC_ASG_WG=2 selects the 320-thread form
+    static const int env_wg = getenv("AC_ASG_WG") ? atoi(getenv("AC_ASG_WG")) : 3;
+    const int nwg = env_wg == 2 ? 2 : 3;
     if (nwg == 2) {
       if (d == 64) k_assign_tc<64, 2><<<grid, threads_for(2), prm.lay.smem, st>>>(prm, probs + p0);
       else k_assign_tc<128, 2><<<grid, threads_for(2), prm.lay.smem, st>>>(prm, probs + p0);
