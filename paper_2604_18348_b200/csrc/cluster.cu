@@ -914,11 +914,16 @@ k_update_w(const ac_cluster_problem* __restrict__ probs, int d, double tol, int 
     if (b < nb) {
       const int base = b * kUpdWRows;
       const int rows = min(kUpdWRows, cnt - base);
-      unsigned char* dst = ring + (size_t)(b % kUpdWStages) * stage_bytes;
-      for (int e = lane; e < kUpdWRows * cpr; e += 32) {
-        const int r = e / cpr, part = e - r * cpr;
+      // lane = (row `sub` of RPI rows, 16-byte piece `part`) per iteration
+      constexpr int RPI = 32 / cpr;
+      const int sub = lane / cpr, part = lane % cpr;
+      unsigned char* dst = ring + (size_t)(b % kUpdWStages) * stage_bytes + sub * row_bytes + part * 16;
+      const char* src = xb + part * 16;
+#pragma unroll 4
+      for (int it = 0; it < kUpdWRows / RPI; ++it) {
+        const int r = it * RPI + sub;
         const int row = __shfl_sync(0xffffffffu, myidx, r);
-        if (r < rows) cp_async16(dst + r * row_bytes + part * 16, xb + (int64_t)row * row_bytes + part * 16);
+        if (r < rows) cp_async16(dst + it * RPI * row_bytes, src + (int64_t)row * row_bytes);
       }
     }
     cp_async_commit();
