@@ -330,8 +330,7 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
         const uint64_t sc = pk2(scale_log2, scale_log2);
         const uint64_t nm = pk2(-m_run, -m_run);
         uint64_t acc0 = pk2(0.f, 0.f), acc1 = pk2(0.f, 0.f);
-#pragma unroll
-        for (int ch = 0; ch < BN / 32; ++ch) {
+        auto exp_chunk = [&](int ch) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const uint64_t x =
@@ -349,6 +348,21 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
             sr[ch][i] = pack_bf16(p0, p1);  // packed P overwrites consumed S slots
           }
           tmem_st16(tP + ch * 16, sr[ch]);
+        };
+        if (nk == BN) {
+#pragma unroll
+          for (int ch = 0; ch < BN / 32; ++ch) exp_chunk(ch);
+        } else {  // the run's last tile: 32-key chunks past its end get P = 0, no exponentials
+#pragma unroll
+          for (int ch = 0; ch < BN / 32; ++ch) {
+            if (ch * 32 < nk) {
+              exp_chunk(ch);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) sr[ch][i] = 0u;
+              tmem_st16(tP + ch * 16, sr[ch]);
+            }
+          }
         }
         float a0, a1, b0, b1;
         up2(acc0, a0, a1);
