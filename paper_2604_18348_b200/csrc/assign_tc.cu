@@ -8,30 +8,32 @@
 // flipped near-tie cascades — SURVEY.md §7 hard part 1).  Design:
 //
 //   1. e_c = ||c||^2 - 2 x·c on tcgen05 (kind::f16, f32 accumulation in
-//      TMEM).  Centres enter as three bf16 planes of -2c (exact split of
-//      f32), ||c||^2 as a 3-way split picked up by one extra K=16 MMA against
-//      a constant ones block; bf16 points are one exact plane (1 + 3 MMA
-//      groups per tile), f32 points arrive as their exact hi/mid/lo bf16
-//      planes (written once per Lloyd run by ac_lloyd_prepare; 1 + 6 groups,
-//      every plane product down to 2^-16 relative).
+//      TMEM), D = 64 or 128 (D/64 SWIZZLE_128B K-atoms per row).  Centres
+//      enter as three bf16 planes of -2c (exact split of f32), ||c||^2 as a
+//      3-way split picked up by one extra K=16 MMA against a constant ones
+//      block (SWIZZLE_32B operands); bf16 points are one exact plane (x times
+//      the three centre planes), f32 points arrive as their exact hi/mid/lo
+//      bf16 planes (written by the fused normalisation pass or
+//      ac_lloyd_prepare) and the MMA runs the three largest products
+//      hi·hi, hi·mid, mid·hi (all six with AC_ASG_F32_TERMS=6).
 //   2. Epilogue, one thread per row (= TMEM lane): e_min and the candidate
-//      mask e_c <= d~_min + 2T - ||x||^2 straight from TMEM, where T bounds
-//      |d~ - d_ref| rigorously (split + accumulation error and the reference
-//      chain's own rounding, both <= c·u·(||x||·||c|| + ||c||^2)).
-//   3. Candidates are recomputed with the reference's exact sequential
-//      fmaf chain (x and c reconstructed exactly from shared memory) and the
-//      first-index minimum of the exact values wins.  Almost every row has
-//      one candidate — its exact d is what `best` (inertia, repair, stage
-//      MSE) needs anyway; a warp's extra candidates are spread over its lanes.
+//      mask e_c <= d~_min + 2.5T - ||x||^2 straight from TMEM, where T bounds
+//      |d~ - d_ref| for every column (dropped split products, tensor-core
+//      accumulation and the reference chain's own rounding).
+//   3. Candidates of rows with more than one (every row's, when the caller
+//      needs exact `best`) are recomputed with the reference's exact
+//      sequential fmaf chain (x and c reconstructed exactly from shared
+//      memory), one (row, candidate) per lane in a warp-wide pass, and the
+//      first-index minimum of the exact values wins.
 //
 // So labels and distances equal k_assign_seq's (the all-FFMA kernel) bit
 // for bit; tests/test_assign_tc.py checks exactly that, on adversarial ties.
 //
-// Warp roles (320 threads, one CTA per SM, persistent over the tiles of a
-// batch of problems):
+// Warp roles (448 threads = NWG 3, or 320 = NWG 2; one CTA per SM, persistent
+// over the tiles of a batch of problems):
 //   warp 0      TMA producer: 128-row x tiles (1 or 3 planes) into a ring
-//   warp 1      MMA issuer (single thread), TMEM owner (2 x 128 columns)
-//   warps 2-9   two epilogue warpgroups, alternating tiles (one TMEM
+//   warp 1      MMA issuer (single thread), TMEM owner (NWG x 128 columns)
+//   warps 2..   NWG epilogue warpgroups, taking tiles round-robin (one TMEM
 //               accumulator each): argmin, exact fix-up, labels / best /
 //               per-tile label histogram (the tiling matches k_scatter).
 // Compiled with --fmad=false: the fix-up reproduces numpy's unfused ops.
