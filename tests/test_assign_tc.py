@@ -104,14 +104,16 @@ def test_tc_assign_degenerate_rows(gpu):
     _compare([x.cuda()], [c.cuda()])
 
 
-def test_tc_assign_merge(gpu):
+@pytest.mark.parametrize("dtype,d", [("bf16", 64), ("bf16", 128), ("f32", 64), ("f32", 128)])
+def test_tc_assign_merge(gpu, dtype, d):
     """Running multi-stage assignment: merge new centres [c_lo, k) into the
     existing (label, best) with strict '<' (earlier centres win ties)."""
     from paper_2604_18348_b200 import _lib as L
-    g = torch.Generator().manual_seed(11)
-    x = (torch.randn(9000, 64, generator=g) * 30).bfloat16().cuda()
-    c_old = torch.randn(100, 64, generator=g) * 30
-    c_new = torch.cat([c_old[:7], torch.randn(93, 64, generator=g) * 30])  # 7 exact duplicates
+    g = torch.Generator().manual_seed(11 + d)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    x = (torch.randn(9000, d, generator=g) * 30).to(tdt).cuda()
+    c_old = torch.randn(100, d, generator=g) * 30
+    c_new = torch.cat([c_old[:7], torch.randn(93, d, generator=g) * 30])  # 7 exact duplicates
     both = torch.cat([c_old, c_new]).cuda()
     lab, best, _, _ = _run([x], [both[:100].contiguous()], L.ASSIGN_MODE_EXACT)
     _compare([x], [both.contiguous()], c_lo=100, merge_from=(lab, best))
