@@ -47,6 +47,8 @@ CONFIGS = {
     "c1": dict(name="C1 2x64 L=4096 f32", heads=2, seq=4096, dim=64, dtype="f32"),
     "c3": dict(name="C3 Wan-2.1-1.3B layer", heads=12, seq=32760, dim=128, dtype="bf16"),
     "c4": dict(name="C4 HunyuanVideo layer", heads=24, seq=118800, dim=128, dtype="bf16"),
+    # one layer of the C5 40-layer stack (per-layer work; the stack is 40x)
+    "c5": dict(name="C5 Wan-2.1-14B layer (1 of 40)", heads=40, seq=75600, dim=128, dtype="bf16"),
 }
 DRIFT = 5e-4
 
