@@ -51,6 +51,9 @@ constexpr uint32_t COL_S = 0, COL_O = 256, COL_P = 384;
 #ifndef AC_FA4_ORDER
 #define AC_FA4_ORDER 1  // MMA issue order per K tile (0: S0 S1 PV0 PV1, 1: S0 PV0 S1 PV1)
 #endif
+#ifndef AC_FA4_LATE_WAIT
+#define AC_FA4_LATE_WAIT 1  // wait for PV_t(j-1) after the exponentials (P kept in registers)
+#endif
 #ifndef AC_FA4_POLY
 #define AC_FA4_POLY 0  // of every 8 exp2 pairs, this many on the FMA pipe (polynomial)
 #endif
@@ -313,11 +316,13 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
               mx[a] = fmaxf(mx[a], fmaxf(__uint_as_float(sr[ch][u + 2 * a]),
                                          __uint_as_float(sr[ch][u + 2 * a + 1])));
         const float ms = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
+#if !AC_FA4_LATE_WAIT
         // P_t / O_t are free once the previous tile's PV has completed
         if (j > 0) {
           mbar_wait_sleep(o_done + t, (j - 1) & 1, 45);
           fence_after();
         }
+#endif
         // lazy rescale: a row's running max only moves when it grows by > 2^8
         const bool need = ms > m_run + 8.f;
         const bool warp_need = __any_sync(0xffffffffu, need);
@@ -347,7 +352,9 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
             else acc0 = add2(acc0, pk2(p0, p1));
             sr[ch][i] = pack_bf16(p0, p1);  // packed P overwrites consumed S slots
           }
+#if !AC_FA4_LATE_WAIT
           tmem_st16(tP + ch * 16, sr[ch]);
+#endif
         };
         if (nk == BN) {
 #pragma unroll
@@ -360,10 +367,22 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
             } else {
 #pragma unroll
               for (int i = 0; i < 16; ++i) sr[ch][i] = 0u;
+#if !AC_FA4_LATE_WAIT
               tmem_st16(tP + ch * 16, sr[ch]);
+#endif
             }
           }
         }
+#if AC_FA4_LATE_WAIT
+        // P_t / O_t are free once the previous tile's PV has completed: the
+        // exponentials above ran while PV_t(j-1) was still on the tensor core
+        if (j > 0) {
+          mbar_wait_sleep(o_done + t, (j - 1) & 1, 45);
+          fence_after();
+        }
+#pragma unroll
+        for (int ch = 0; ch < BN / 32; ++ch) tmem_st16(tP + ch * 16, sr[ch]);
+#endif
         float a0, a1, b0, b1;
         up2(acc0, a0, a1);
         up2(acc1, b0, b1);

@@ -1276,6 +1276,40 @@ __global__ void k_kpp_dist(const ac_cluster_problem* __restrict__ probs, int dty
   P.best[r] = (s == 0) ? dist : np_minimum(P.best[r], dist);
 }
 
+// D = 64 / 128 form of k_kpp_dist: 8 lanes per row, lane j runs numpy's
+// pairwise accumulator r_j = sum_m (x[j+8m] - c[j+8m])^2 in order and
+// pw8_combine folds the 8 (same operations as pw_sum, same bits); each load
+// instruction of a warp touches 4 rows x 8 consecutive elements.
+template <int D>
+__global__ void __launch_bounds__(256)
+k_kpp_dist_v(const ac_cluster_problem* __restrict__ probs, int dtype, int s) {
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  if (s + 1 >= P.k || P.status[AC_ST_KPP_STOP] >= 0) return;
+  const int j = threadIdx.x & 7;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3);
+  const bool ok = r < P.n;
+  const int64_t base = (ok ? r : 0) * D;
+  const float* c = P.centers + (int64_t)s * D;
+  float xv[D / 8];
+  if (dtype == AC_DTYPE_BF16) {
+    const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(P.x) + base;
+#pragma unroll
+    for (int m = 0; m < D / 8; ++m) xv[m] = __bfloat162float(x[j + 8 * m]);
+  } else {
+    const float* x = reinterpret_cast<const float*>(P.x) + base;
+#pragma unroll
+    for (int m = 0; m < D / 8; ++m) xv[m] = __ldg(x + j + 8 * m);
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int m = 0; m < D / 8; ++m) {
+    const float df = __fsub_rn(xv[m], c[j + 8 * m]);
+    acc = m == 0 ? __fmul_rn(df, df) : __fadd_rn(acc, __fmul_rn(df, df));
+  }
+  const float dist = pw8_combine(acc);
+  if (ok && j == 0) P.best[r] = (s == 0) ? dist : np_minimum(P.best[r], dist);
+}
+
 // total = closest.sum(); p = closest / total; choice(n, p): f64 cumsum,
 // /= cdf[-1], searchsorted(u, 'right').  One CTA of 1024 threads per problem.
 // The f64 prefix sums are computed in parallel; they equal numpy's sequential
@@ -1987,9 +2021,16 @@ extern "C" int ac_kmeanspp(const ac_cluster_problem* probs, int nprob, int dtype
   const size_t psm = plan_vals_bytes(max_n, sizeof(float));
   int rc = set_smem((const void*)k_kpp_pick, psm);
   if (rc) return rc;
+  const bool rows_fast = (d == 64 || d == 128) && (dtype == AC_DTYPE_F32 || dtype == AC_DTYPE_BF16);
   for (int s = 0; s + 1 < max_k; ++s) {
-    k_kpp_dist<<<dim3((unsigned)((max_n + 255) / 256), nprob), 256, sizeof(float) * d, st>>>(
-        probs, dtype, d, s);
+    if (rows_fast) {
+      const dim3 grid((unsigned)((max_n + 31) / 32), nprob);
+      if (d == 64) k_kpp_dist_v<64><<<grid, 256, 0, st>>>(probs, dtype, s);
+      else k_kpp_dist_v<128><<<grid, 256, 0, st>>>(probs, dtype, s);
+    } else {
+      k_kpp_dist<<<dim3((unsigned)((max_n + 255) / 256), nprob), 256, sizeof(float) * d, st>>>(
+          probs, dtype, d, s);
+    }
     k_kpp_pick<<<nprob, 1024, psm, st>>>(probs, dtype, d, s, draws, max_k);
   }
   AC_CHECK_LAUNCH("ac_kmeanspp");
