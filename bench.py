@@ -297,6 +297,18 @@ def main():
     del steps
     params = _params(P)
     from paper_2604_18348_b200.sharding import ShardedLayerSession, gather_heads
+
+    # process warm-up: the first step-0 of a process also pays one-off costs
+    # (library/module load, allocator growth, tensor maps); the reported
+    # cold_step_ms is a fresh session's step 0 after it
+    first = ShardedLayerSession(H, params, seed=0, layer=0, out_dtype=tdt)
+    torch.cuda.synchronize()
+    tf = time.perf_counter()
+    first.session.step(*dev_in[0])
+    torch.cuda.synchronize()
+    cold_first_ms = (time.perf_counter() - tf) * 1e3
+    del first
+    torch.cuda.empty_cache()
     shard = ShardedLayerSession(H, params, seed=0, layer=0, out_dtype=tdt)
     sess = shard.session
     sess.attn_impl = args.attn_impl
@@ -429,6 +441,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "cold_step_ms": cold_ms,
+            "cold_step_first_in_process_ms": cold_first_ms,
             "phases_ms_eager_step": phases,
             "dense_sdpa_ms": dense,
             "density": sess.density(),

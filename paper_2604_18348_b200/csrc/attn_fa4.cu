@@ -13,15 +13,18 @@
 //   warps 0-3   softmax of Q tile 0 (thread = query row = TMEM lane)
 //   warps 4-7   softmax of Q tile 1
 //   warp 8      TMA producer: Q0/Q1 once, K/V tiles through a 4-stage ring
-//   warp 9      MMA issuer: S_t = Q_t·Kᵀ into TMEM (kind::f16, f32 accum),
-//               O_t += P_t·V with P_t read from TMEM (the A-from-TMEM form)
+//   warps 9/10  MMA issuers, one per Q tile: S_t = Q_t·Kᵀ into TMEM
+//               (kind::f16, f32 accum), O_t += P_t·V with P_t read from TMEM
+//               (the A-from-TMEM form); a K/V stage is released when both
+//               tiles' PV on it have completed
 // TMEM (512 columns): S0 | S1 (128 each) | O0 | O1 (64 each) | P0 | P1
 // (64 x 32-bit columns = 128 bf16 each).  While one tile's softmax runs the
 // tensor core works on the other tile's S or PV.
 // Softmax in the exp2 domain with lazy rescaling (the running max only
-// moves when a row max grows by more than 2^8); ~3/8 of the exponentials
+// moves when a row max grows by more than 2^8); 1/8 of the exponentials
 // are evaluated with a cubic polynomial on the FMA pipe (packed f32x2) to
-// offload the MUFU unit, which otherwise bounds D = 64 attention on B200.
+// offload the MUFU unit, which otherwise bounds D = 64 attention on B200
+// (2/8 measured slower: the softmax warps are then issue-limited).
 // Epilogue: O / l, bf16 or f32, stored at the query's original token row
 // (the inverse permutation is fused into the store).
 #include <cfloat>
@@ -36,8 +39,15 @@ constexpr int D = 64;
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int STAGES = 4;
+#ifndef AC_FA4_SPLIT_MMA
+#define AC_FA4_SPLIT_MMA 1  // one MMA-issuing warp per Q tile (no head-of-line blocking)
+#endif
+#if AC_FA4_SPLIT_MMA
+constexpr int THREADS = 352;
+#else
 constexpr int THREADS = 320;
-constexpr int W_TMA = 8, W_MMA = 9;
+#endif
+constexpr int W_TMA = 8, W_MMA = 9, W_MMA1 = 10;
 constexpr int Q_BYTES = BM * D * 2;
 constexpr int KV_BYTES = BN * D * 2;
 constexpr int OFF_Q = 0;
@@ -55,7 +65,7 @@ constexpr uint32_t COL_S = 0, COL_O = 256, COL_P = 384;
 #define AC_FA4_LATE_WAIT 1  // wait for PV_t(j-1) after the exponentials (P kept in registers)
 #endif
 #ifndef AC_FA4_POLY
-#define AC_FA4_POLY 0  // of every 8 exp2 pairs, this many on the FMA pipe (polynomial)
+#define AC_FA4_POLY 1  // of every 8 exp2 pairs, this many on the FMA pipe (polynomial)
 #endif
 
 AC_DEV void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
@@ -174,7 +184,7 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
     mbar_init(q_full, 1);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(kv_full + s, 1);
-      mbar_init(kv_empty + s, 1);
+      mbar_init(kv_empty + s, (AC_FA4_SPLIT_MMA && two) ? 2 : 1);
     }
     for (int t = 0; t < 2; ++t) {
       // only warps holding at least one real query row take part (the rest
@@ -213,6 +223,52 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
       }
     }
     __syncwarp();
+#if AC_FA4_SPLIT_MMA
+  } else if (warp == W_MMA || warp == W_MMA1) {
+    // ------------------- MMA issuers: one warp per Q tile -----------------------
+    // Each tile's S/PV chain only waits for its own softmax; a K/V stage is
+    // released once every tile's PV on it has completed (kv_empty count).
+    const int t = warp - W_MMA;
+    if (lane == 0 && (t == 0 || two)) {
+      constexpr uint32_t IS = idesc_bf16(BM, BN, false);
+      constexpr uint32_t IO = idesc_bf16(BM, D, true);
+      const uint32_t sq = smem_u32(sm + OFF_Q) + t * Q_BYTES;
+      auto issue_pv = [&](int jj, int st, bool release) {
+        mbar_wait_sleep(p_full + t, jj & 1, 41);
+        fence_after();
+        const uint32_t sv = smem_u32(sm + OFF_V + st * KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t bd = sdesc(sv + kk * 2048, BN * 128, 1024);
+          umma_ts(tmem + COL_O + t * D, tmem + COL_P + t * 64 + kk * 8, bd, IO,
+                  (jj > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(o_done + t);
+        if (release) umma_commit(kv_empty + st);
+      };
+      mbar_wait_sleep(q_full, 0, 42);
+      TileIter ti(iruns, it.nruns);
+      int start, nk, j = 0;
+      while (ti.next(start, nk)) {
+        const int st = j % STAGES;
+        mbar_wait_sleep(kv_full + st, (j / STAGES) & 1, 43);
+        fence_after();
+        if (j > 0) mbar_wait_sleep(s_free + t, (j - 1) & 1, 47);
+        const uint32_t sk = smem_u32(sm + OFF_K + st * KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t ad = sdesc(sq + kk * 32, 16, 1024);
+          const uint64_t bd = sdesc(sk + kk * 32, 16, 1024);
+          umma_f16(tmem + COL_S + t * BN, ad, bd, IS, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full + t);
+        if (j > 0) issue_pv(j - 1, (j - 1) % STAGES, true);
+        ++j;
+      }
+      if (j > 0) issue_pv(j - 1, (j - 1) % STAGES, false);
+    }
+    __syncwarp();
+#else
   } else if (warp == W_MMA) {
     // ------------------------------ MMA issuer --------------------------------
     if (lane == 0) {
@@ -275,6 +331,7 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
       }
     }
     __syncwarp();
+#endif
   } else {
     // ------------------------------ softmax ------------------------------
     const int t = warp >> 2;  // Q tile of this warpgroup
