@@ -11,7 +11,8 @@ d = dict(zip(h, v))
 def g(k, default="?"):
     return d.get(k, default)
 print(f"kernel: {g('Kernel Name')[:100]}")
-print(f"duration_us: {g('gpu__time_duration.sum')}  grid: {g('launch__grid_size')}  block: {g('launch__block_size')}  regs: {g('launch__registers_per_thread')}")
+units = dict(zip(h, raw[1]))
+print(f"duration: {g('gpu__time_duration.sum')} {units.get('gpu__time_duration.sum', '')}  grid: {g('launch__grid_size')}  block: {g('launch__block_size')}  regs: {g('launch__registers_per_thread')}")
 rd = float(g('dram__bytes_read.sum', 0) or 0); wr = float(g('dram__bytes_write.sum', 0) or 0)
 unit = [u for k, u in zip(h, raw[1]) if k == 'dram__bytes_read.sum']
 print(f"dram_bytes_read: {rd} {unit[0] if unit else ''}  dram_bytes_write: {wr}")
