@@ -38,7 +38,10 @@ using namespace ac::tc;
 constexpr int D = 64;
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int STAGES = 4;
+#ifndef AC_FA4_STAGES
+#define AC_FA4_STAGES 4
+#endif
+constexpr int STAGES = AC_FA4_STAGES;
 #ifndef AC_FA4_SPLIT_MMA
 #define AC_FA4_SPLIT_MMA 1  // one MMA-issuing warp per Q tile (no head-of-line blocking)
 #endif
