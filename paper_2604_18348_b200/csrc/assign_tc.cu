@@ -65,7 +65,9 @@ constexpr float kPadE = 3.0e38f;        // e of the padding columns (never a can
 // Shared-memory layout, sized per launch from the largest centre count
 // (cap = max round16(k - c_lo)):
 //   x stages   XS x NP planes x [128 rows][64] bf16 (SW128, TMA-written);
-//              NP = 1 for bf16 points (exact), 3 for f32 points (hi/mid/lo)
+//              NP = 1 for bf16 points (exact), 2 for f32 points (hi/mid: the
+//              planes the three-product MMA reads; exact chains read the f32
+//              row from global memory), 3 (hi/mid/lo) in the six-product form
 //   centres    3 planes of -2c [cap][64] bf16 (SW128)
 //   aug        A: [128][64] bf16 with columns 0..2 = 1;  B: [cap][64] with
 //              columns 0..2 = the exact 3-way split of ||c||^2  -> one extra
@@ -90,10 +92,24 @@ struct Params {
 
 // D = 64: exact f32 centres in shared memory; D = 128: the exact centres
 // are re-joined from the -2c planes (no room for both)
-__host__ __device__ inline Layout make_layout(int dtype, int dim, int cap, int xs) {
+#ifndef AC_ASG_X_GLOBAL
+#define AC_ASG_X_GLOBAL 1  // 3-product f32 form: stage hi/mid only, exact chains read the f32 row
+#endif
+inline int f32_terms_env() {
+  static const int t = getenv("AC_ASG_F32_TERMS") ? atoi(getenv("AC_ASG_F32_TERMS")) : 3;
+  return t == 6 ? 6 : 3;
+}
+// bf16 planes of x staged per tile: bf16 points 1; f32 points hi/mid (the
+// planes the three-product MMA reads; the exact chains then read the f32
+// row from global memory) or hi/mid/lo (six products, or AC_ASG_X_GLOBAL=0)
+__host__ __device__ inline int x_planes(int dtype, int terms) {
+  if (dtype != AC_DTYPE_F32) return 1;
+  return (AC_ASG_X_GLOBAL && terms != 6) ? 2 : 3;
+}
+__host__ __device__ inline Layout make_layout(int dtype, int dim, int cap, int xs, int terms) {
   Layout l;
   const int kb = dim / 64;
-  l.np = dtype == AC_DTYPE_F32 ? 3 : 1;
+  l.np = x_planes(dtype, terms);
   l.xs = xs;
   l.stage_bytes = l.np * kb * ATOM;
   l.off_cp = l.xs * l.stage_bytes;
@@ -153,7 +169,8 @@ AC_DEV void join8(const uint4& h, const uint4& m, const uint4& l, float (&v)[8])
 // (D = 64) or re-joined from the -2c planes (exact, times -1/2).
 template <int DIM>
 AC_DEV float exact_dist(const unsigned char* xsm, bool f32in, int r, const float* cf,
-                        const unsigned char* cp, int cpb, int cap, int c, float xx, float cc) {
+                        const unsigned char* cp, int cpb, int cap, int c, float xx, float cc,
+                        const float* __restrict__ xg = nullptr) {
   constexpr int PLB = BM * DIM * 2;
   constexpr int UNR = DIM == 64 ? 8 : 2;  // bounded register footprint at D = 128
   float acc = 0.f;
@@ -161,7 +178,12 @@ AC_DEV float exact_dist(const unsigned char* xsm, bool f32in, int r, const float
   for (int j = 0; j < DIM / 8; ++j) {
     const int off = (j >> 3) * ATOM + sw128(r, j & 7);
     float xv[8];
-    if (f32in) {
+    if (xg) {  // the f32 row itself (global memory / L2)
+      const float4 a = __ldg(reinterpret_cast<const float4*>(xg + 8 * j));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(xg + 8 * j + 4));
+      xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
+      xv[4] = b.x; xv[5] = b.y; xv[6] = b.z; xv[7] = b.w;
+    } else if (f32in) {
       join8(*reinterpret_cast<const uint4*>(xsm + off),
             *reinterpret_cast<const uint4*>(xsm + PLB + off),
             *reinterpret_cast<const uint4*>(xsm + 2 * PLB + off), xv);
@@ -464,6 +486,7 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
         // all 32 lanes of the warp (a row whose single candidate is already
         // decided needs none when only labels are asked for)
         const unsigned char* xsm = sm + s * SB;
+        const float* xglob = (f32in && NP == 2) ? reinterpret_cast<const float*>(P.x) : nullptr;
         const bool lonly = (prm.flags & AC_ASSIGN_LABELS_ONLY) != 0;
         float best = INFINITY;
         int lbl = INT_MAX;
@@ -501,7 +524,8 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
               const float xs = __shfl_sync(0xffffffffu, xx, src);
               if (e2 < total)
                 qr[e2] = exact_dist<DIM>(xsm, f32in, q * 32 + src, cf32 + c * CF_STRIDE, cplanes, CPB,
-                                         CPB / (KB * 128), c, xs, s_cc[c]);
+                                         CPB / (KB * 128), c, xs, s_cc[c],
+                                         xglob ? xglob + ((int64_t)tile * BM + q * 32 + src) * DIM : nullptr);
             }
             __syncwarp();
             for (int e2 = off; e2 < off + cnt; ++e2) {  // ascending centre order, first wins
@@ -517,7 +541,8 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
                 const int c = ch * 32 + __ffs(m) - 1;
                 m &= m - 1;
                 const float d = exact_dist<DIM>(xsm, f32in, r, cf32 + c * CF_STRIDE, cplanes, CPB,
-                                                CPB / (KB * 128), c, xx, s_cc[c]);
+                                                CPB / (KB * 128), c, xx, s_cc[c],
+                                                xglob ? xglob + row * DIM : nullptr);
                 if (d < best) { best = d; lbl = c; }
               }
             }
@@ -600,7 +625,8 @@ bool assign_tc_eligible(const ac_cluster_problem* host_probs, int nprob, int dty
   }
   for (int p0 = 0; p0 < nprob; p0 += ac::asg::MAXP) {
     const int cap = tc_cap(host_probs + p0, std::min(ac::asg::MAXP, nprob - p0), c_lo);
-    if (ac::asg::make_layout(dtype, d, cap, 1).smem > ac::asg::SMEM_MAX) return false;
+    if (ac::asg::make_layout(dtype, d, cap, 1, ac::asg::f32_terms_env()).smem > ac::asg::SMEM_MAX)
+      return false;
   }
   return true;
 }
@@ -625,8 +651,9 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     memset(&prm, 0, sizeof(prm));
     const int cap = tc_cap(host_probs + p0, np, c_lo);
     int xs = 4;
-    while (xs > 1 && make_layout(dtype, d, cap, xs).smem > SMEM_MAX) --xs;
-    prm.lay = make_layout(dtype, d, cap, xs);
+    prm.f32_terms = f32_terms_env();
+    while (xs > 1 && make_layout(dtype, d, cap, xs, prm.f32_terms).smem > SMEM_MAX) --xs;
+    prm.lay = make_layout(dtype, d, cap, xs, prm.f32_terms);
     if (prm.lay.smem > SMEM_MAX) {
       set_error("k_assign_tc: shared-memory layout %d B exceeds the budget", prm.lay.smem);
       return AC_ERR_PARAM;
@@ -635,8 +662,6 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     prm.dtype = dtype;
     prm.c_lo = c_lo;
     prm.flags = flags;
-    static const int f32_terms = getenv("AC_ASG_F32_TERMS") ? atoi(getenv("AC_ASG_F32_TERMS")) : 3;
-    prm.f32_terms = f32_terms == 6 ? 6 : 3;
     prm.tile0[0] = 0;
     for (int j = 0; j < np; ++j) {
       const ac_cluster_problem& P = host_probs[p0 + j];
@@ -645,7 +670,7 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
       // bf16 points: the tile itself; f32 points: the [3][n][d] planes.
       // Box = one 64-column SW128 atom; the kernel issues d/64 boxes per plane.
       const void* base = dtype == AC_DTYPE_F32 ? P.planes : P.x;
-      const int64_t rows = (dtype == AC_DTYPE_F32 ? 3 : 1) * std::max<int64_t>(P.n, 1);
+      const int64_t rows = (dtype == AC_DTYPE_F32 ? 3 : 1) * std::max<int64_t>(P.n, 1);  // map spans all planes
       int rc = make_map_2d(&prm.x[j], base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, d, 64, BM);
       if (rc) return rc;
     }

@@ -1,12 +1,12 @@
 #!/bin/bash
 # A/B compile-time variants of one attention unit on the GPU box.
-# usage: tools/ab_attn.sh <unit.cu> "<flags A>" "<flags B>" ...   (flags may be "")
+# usage: [AB_NVCC=...] [AB_TEST=...] [AB_CONFIGS=...] tools/ab_attn.sh <unit.cu> "<flags A>" "<flags B>" ...   (flags may be "")
 mkdir -p gpurun_out build/csrc
 unit=$1; shift
 out=gpurun_out/ab_attn.txt; : > $out
 for fl in "$@"; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-    --extended-lambda --expt-relaxed-constexpr -Iinclude $fl -c paper_2604_18348_b200/csrc/$unit \
+    --extended-lambda --expt-relaxed-constexpr -Iinclude $AB_NVCC $fl -c paper_2604_18348_b200/csrc/$unit \
     -o build/csrc/$unit.o || { echo "build failed: $fl" >> $out; continue; }
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_2604_18348_b200/libadacluster_sm100.so \
     build/csrc/*.o -lcudart
