@@ -8,6 +8,7 @@
 // the union of the selected key clusters of g, given as [start, end) runs of
 // the cluster-contiguous Kp/Vp (adjacent selected clusters are merged).
 #include <cfloat>
+#include <climits>
 
 #include "common.cuh"
 
@@ -104,6 +105,26 @@ __global__ void k_q_layout_rows(const void* __restrict__ q, int dtype, int d, in
   } else {
     for (int o = 0; o < bytes; ++o) op[o] = sp[o];
   }
+}
+
+// the same scatter with one thread per 16-byte piece (rows of 16-byte
+// multiples, 16-byte aligned bases): a warp moves whole contiguous rows
+__global__ void k_q_layout_rows16(const uint4* __restrict__ q, int pieces, int64_t L,
+                                  const int32_t* __restrict__ qperm, const int32_t* __restrict__ qstarts,
+                                  const int32_t* __restrict__ qlabels, int gq_max,
+                                  const int32_t* __restrict__ padstart, uint4* __restrict__ qp,
+                                  int32_t* __restrict__ qidx, int64_t qp_cap) {
+  const int h = blockIdx.y;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;  // L * pieces < 2^31 (host check)
+  const int j = e / pieces;
+  const int part = e - j * pieces;
+  if (j >= L) return;
+  const int32_t tok = qperm[(int64_t)h * L + j];
+  const int g = qlabels[(int64_t)h * L + tok];
+  const int64_t local = j - qstarts[(int64_t)h * (gq_max + 1) + g];
+  const int64_t row = (int64_t)h * qp_cap + padstart[(int64_t)h * gq_max + g] + local;
+  if (part == 0) qidx[row] = tok;
+  qp[row * pieces + part] = __ldg(q + ((int64_t)h * L + tok) * pieces + part);
 }
 
 // ---------------------------------------------------------------------------
@@ -312,8 +333,17 @@ extern "C" int ac_build_q_layout(const void* q, int dtype, int d, int64_t L, int
   cudaMemsetAsync(qidx, 0xff, sizeof(int32_t) * (size_t)heads * qp_cap, st);
   k_q_layout_items<<<heads, 32, 0, st>>>(L, qcounts, gq, gq_max, nruns, topk_max, qp_cap, padstart,
                                          items, item_cap, item_rows);
-  k_q_layout_rows<<<dim3((unsigned)((L + 255) / 256), heads), 256, 0, st>>>(
-      q, dtype, d, L, qperm, qstarts, qlabels, gq_max, padstart, qp, qidx, qp_cap);
+  const int bytes = d * (dtype == AC_DTYPE_BF16 ? 2 : 4);
+  if ((bytes & 15) == 0 && L * (bytes / 16) < (int64_t)INT_MAX - 256 &&
+      ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(qp)) & 15) == 0) {
+    const int pieces = bytes / 16;
+    k_q_layout_rows16<<<dim3((unsigned)((L * pieces + 255) / 256), heads), 256, 0, st>>>(
+        reinterpret_cast<const uint4*>(q), pieces, L, qperm, qstarts, qlabels, gq_max, padstart,
+        reinterpret_cast<uint4*>(qp), qidx, qp_cap);
+  } else {
+    k_q_layout_rows<<<dim3((unsigned)((L + 255) / 256), heads), 256, 0, st>>>(
+        q, dtype, d, L, qperm, qstarts, qlabels, gq_max, padstart, qp, qidx, qp_cap);
+  }
   AC_CHECK_LAUNCH("ac_build_q_layout");
   return AC_OK;
 }
