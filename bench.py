@@ -59,7 +59,7 @@ def _params(P):
 
 def gen_head(cfg, h: int):
     """Two consecutive steps of head h (per-head seed 1000 + h)."""
-    from paper_2604_18348_b200.synthetic import CRIT7_SPEC, gen_synthetic
+    from workload.synthetic import CRIT7_SPEC, gen_synthetic
     spec = dataclasses.replace(CRIT7_SPEC, drift_sigma=DRIFT)
     return gen_synthetic(spec, cfg["seq"], cfg["dim"], 1, 2, 1000 + h)
 

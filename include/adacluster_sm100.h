@@ -355,12 +355,6 @@ int ac_sparse_attention_fa4_d128(const void* q, int64_t q_rows_total,
                                  const ac_attn_item* items, int nitems,
                                  const int32_t* runs, float scale, void* out,
                                  int out_dtype, void* stream);
-int ac_sparse_attention_tc(const void* q, int64_t q_rows_total,
-                           const int32_t* qidx, const void* k, const void* v,
-                           int d, int64_t L, int heads,
-                           const ac_attn_item* items, int nitems,
-                           const int32_t* runs, float scale, void* out,
-                           int out_dtype, void* stream);
 
 #ifdef __cplusplus
 }

@@ -33,7 +33,6 @@ UNITS = {
     "cluster.cu": ["--fmad=false"],
     "select.cu": ["--fmad=false"],
     "attn_simt.cu": [],
-    "attn_tc.cu": [],
     "attn_fa4.cu": [],
     "attn_fa4_d128.cu": [],
     "assign_tc.cu": ["--fmad=false"],

@@ -1,5 +1,5 @@
 // tcgen05 / TMA / mbarrier helpers shared by the sm_100a tensor-core kernels
-// (attn_tc.cu, assign_tc.cu).  Inline PTX only; compiled for sm_100a.
+// (attn_fa4*.cu, assign_tc.cu).  Inline PTX only; compiled for sm_100a.
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>

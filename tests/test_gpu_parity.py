@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2604_18348_b200.synthetic import CRIT7_SPEC, LayerSpec, gen_synthetic
+from workload.synthetic import CRIT7_SPEC, LayerSpec, gen_synthetic
 
 pytestmark = pytest.mark.gpu
 

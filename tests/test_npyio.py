@@ -117,7 +117,7 @@ def test_load_layer_drives_the_layer_step(gpu, tmp_path):
     device tensors (bf16) and the same layer output as the in-memory inputs."""
     import torch
     from paper_2604_18348_b200.npyio import load_layer
-    from paper_2604_18348_b200.synthetic import CRIT7_SPEC, gen_synthetic
+    from workload.synthetic import CRIT7_SPEC, gen_synthetic
     H, L, D = 2, 3000, 64
     steps = [[[tuple(a) for a in (gen_synthetic(CRIT7_SPEC, L, D, 1, 1, 10 + h)[0][0] for h in range(H))]]]
     write_dump(tmp_path, steps)

@@ -8,7 +8,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from paper_2604_18348_b200.synthetic import CRIT7_SPEC, LayerSpec, gen_synthetic
+from workload.synthetic import CRIT7_SPEC, LayerSpec, gen_synthetic
 
 G = Path(__file__).resolve().parent / "golden"
 

@@ -6,7 +6,7 @@ import dataclasses
 import pytest
 import torch
 
-from paper_2604_18348_b200.synthetic import CRIT7_SPEC, gen_synthetic
+from workload.synthetic import CRIT7_SPEC, gen_synthetic
 
 pytestmark = pytest.mark.gpu
 

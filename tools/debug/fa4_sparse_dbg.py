@@ -1,7 +1,7 @@
 import sys, torch, numpy as np
 sys.path.insert(0, '.')
 import paper_2604_18348_b200 as P
-from paper_2604_18348_b200.synthetic import CRIT7_SPEC, gen_synthetic
+from workload.synthetic import CRIT7_SPEC, gen_synthetic
 q, k, v = gen_synthetic(CRIT7_SPEC, 8192, 64, 1, 1, 0)[0][0]
 Q, K, V = (torch.from_numpy(a).bfloat16().cuda()[None] for a in (q, k, v))
 params = P.PipelineParams(q_clusters=65, topk=25, full_layer_quota=0.0)
