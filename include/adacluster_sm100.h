@@ -129,6 +129,24 @@ int ac_pw_plan_build(int64_t n, int32_t* host_out, int64_t cap);
 /* OpenBLAS dispatch of the reference's f32 `a @ b.T` ([m,d] x [n,d]) */
 int ac_gemm_order(int64_t m, int64_t n, int64_t d);
 
+/* ---- workspace sizing ---------------------------------------------------
+ * Byte size of every caller-owned buffer of one op (returns the total, or -1
+ * with ac_last_error() set).  fields (optional, host, nfields entries) gets the
+ * per-buffer sizes in the order listed; dims (host) by op:
+ *   AC_WS_CLUSTER   {n, kcap, d, dtype, max_iter} -> the 19 buffer fields of
+ *                   ac_cluster_problem in declaration order (xx ... clsb);
+ *                   optional buffers are 0 when the kernels will not use them
+ *   AC_WS_SELECT    {gq, c, topk, run_stride} -> scores, selected, runs,
+ *                   nruns, covered, density of ac_select_problem
+ *   AC_WS_ATTENTION {L, heads, gq_max, topk_max, d, dtype} -> qp, qidx,
+ *                   items, kp, vp of ac_build_q_layout / ac_sparse_attention
+ *                   (runs/nruns are the selection's)                       */
+#define AC_WS_CLUSTER 0
+#define AC_WS_SELECT 1
+#define AC_WS_ATTENTION 2
+int64_t ac_workspace_bytes(int op, const int64_t* dims, int ndims, int64_t* fields,
+                           int nfields);
+
 /* ---- K1 tensorops.py:59-76 l2_normalize_rows ---------------------------
  * out[i] = x[i] / ||x[i]||  (numpy pairwise-8 norm, f32 divide), rows with
  * |norm-1| <= 2e-6 copied unchanged, norm < 1e-12 -> zeros + degenerate[i]=1.
@@ -285,6 +303,20 @@ typedef struct ac_attn_item {
   int32_t run0;          /* first run in the runs table                     */
   int32_t nruns;         /* number of [start,end) runs                       */
 } ac_attn_item;
+
+/* ---- substrate ops (tensorops.py:29-51, quest.py:74-91) ------------------
+ * ac_matmul      out[m, n] = a[m, k] @ b[k, n] (f32) in the OpenBLAS
+ *                accumulation `order` (AC_ORDER_*; ac_gemm_order(m, n, k))
+ * ac_row_softmax out = softmax(scale * s) over the last axis (row-max
+ *                subtraction), rows x cols f32
+ * ac_quest_pairs out[g, c] = sum_t max(q[g,t]*emax[c,t], q[g,t]*emin[c,t]) in
+ *                numpy's pairwise order (the scalar Quest bound, quest_scalar) */
+int ac_matmul(const float* a, int64_t m, int k, const float* b, int64_t n, float* out,
+              int order, void* stream);
+int ac_row_softmax(const float* s, int64_t rows, int64_t cols, float scale, float* out,
+                   void* stream);
+int ac_quest_pairs(const float* q, int gq, int d, const float* emax, const float* emin, int c,
+                   float* out, void* stream);
 
 /* ---- K12 permutation -----------------------------------------------------
  * dst[j] = src[perm[j]] for j < n (row gather, 16-byte vectors)            */

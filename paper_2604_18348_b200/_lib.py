@@ -64,6 +64,10 @@ _SIGS = {
     "ac_pw_plan_len": [_I64],
     "ac_pw_plan_build": [_I64, _P, _I64],
     "ac_gemm_order": [_I64, _I64, _I64],
+    "ac_workspace_bytes": [_I, _P, _I, _P, _I],
+    "ac_matmul": [_P, _I64, _I, _P, _I64, _P, _I, _P],
+    "ac_row_softmax": [_P, _I64, _I64, _F, _P, _P],
+    "ac_quest_pairs": [_P, _I, _I, _P, _P, _I, _P, _P],
     "ac_l2norm": [_P, _I, _I64, _I, _P, _P, _P, _P],
     "ac_l2norm_ex": [_P, _I, _I64, _I, _P, _P, _P, _P, _I64, _P],
     "ac_row_sqnorm": [_P, _I, _I64, _I, _P, _P],
@@ -98,7 +102,7 @@ _SIGS = {
     "ac_sparse_attention_fa4_d128": [_P, _I64, _P, _P, _P, _I, _I64, _I, _P, _I, _P, _F, _P, _I, _P],
     "ac_sparse_attention_simt": [_P, _P, _P, _P, _I, _I, _I64, _P, _I, _P, _F, _P, _I, _P],
 }
-_RESTYPES = {"ac_last_error": ctypes.c_char_p, "ac_pw_plan_len": _I64}
+_RESTYPES = {"ac_last_error": ctypes.c_char_p, "ac_pw_plan_len": _I64, "ac_workspace_bytes": _I64}
 
 EXPORTED = tuple(_SIGS)
 
@@ -172,6 +176,27 @@ def pw_plan(n: int) -> torch.Tensor:
         t = torch.from_numpy(host).to(dev)
         _PLANS[key] = t
     return t
+
+
+WS_CLUSTER, WS_SELECT, WS_ATTENTION = 0, 1, 2
+WS_FIELDS = {
+    WS_CLUSTER: ("xx", "centers", "cc", "labels", "best", "counts", "perm", "starts",
+                 "tile_hist", "inertia", "movement", "status", "plan_n", "plan_k", "dscratch",
+                 "planes", "csum", "cabs", "clsb"),
+    WS_SELECT: ("scores", "selected", "runs", "nruns", "covered", "density"),
+    WS_ATTENTION: ("qp", "qidx", "items", "kp", "vp"),
+}
+
+
+def workspace_bytes(op: int, *dims: int) -> dict:
+    """Per-buffer byte sizes of one problem / launch (ac_workspace_bytes)."""
+    names = WS_FIELDS.get(op, ())
+    d = np.asarray(dims, np.int64)
+    f = np.zeros(max(len(names), 1), np.int64)
+    tot = int(lib().ac_workspace_bytes(op, d.ctypes.data, len(d), f.ctypes.data, len(names)))
+    if tot < 0:
+        check(AC_ERR_PARAM, "ac_workspace_bytes")
+    return dict(zip(names, (int(x) for x in f)))
 
 
 def to_device_struct(arr: np.ndarray) -> torch.Tensor:

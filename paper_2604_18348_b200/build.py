@@ -32,6 +32,7 @@ UNITS = {
     "capi.cu": [],
     "cluster.cu": ["--fmad=false"],
     "select.cu": ["--fmad=false"],
+    "tensorops.cu": ["--fmad=false"],
     "attn_simt.cu": [],
     "attn_fa4.cu": [],
     "attn_fa4_d128.cu": [],

@@ -196,3 +196,87 @@ extern "C" int ac_sparse_attention(const void* q, int64_t q_rows_total, const in
   return ac_sparse_attention_simt(q, qidx, k, v, dtype, d, L, items, nitems, runs, scale, out,
                                   out_dtype, stream);
 }
+
+// ---------------------------------------------------------------------------
+// workspace sizing: byte size of every caller-owned buffer of one problem /
+// one attention launch, so a non-Python caller can size its allocations from
+// the header alone (engine.Batch allocates exactly these; tests/test_abi.py).
+// ---------------------------------------------------------------------------
+namespace {
+int64_t put(int64_t* f, int nf, int i, int64_t v) {
+  if (f && i < nf) f[i] = v;
+  return v;
+}
+}  // namespace
+
+extern "C" int64_t ac_workspace_bytes(int op, const int64_t* dims, int ndims, int64_t* fields,
+                                      int nfields) {
+  auto need = [&](int k) {
+    if (!dims || ndims < k) {
+      ac_host::set_error("ac_workspace_bytes: op %d needs %d dims, got %d", op, k, ndims);
+      return false;
+    }
+    for (int i = 0; i < k; ++i)
+      if (dims[i] < 0) {
+        ac_host::set_error("ac_workspace_bytes: dims[%d] = %lld < 0", i, (long long)dims[i]);
+        return false;
+      }
+    return true;
+  };
+  int64_t tot = 0;
+  if (op == AC_WS_CLUSTER) {
+    if (!need(5)) return -1;
+    const int64_t n = dims[0], kcap = dims[1], d = dims[2], dtype = dims[3], mi = dims[4];
+    const bool fast = (d == 64 || d == 128);
+    const int64_t tiles = (n + 127) / 128;
+    int i = 0;
+    tot += put(fields, nfields, i++, 4 * n);                     // xx
+    tot += put(fields, nfields, i++, 4 * kcap * d);              // centers
+    tot += put(fields, nfields, i++, 4 * kcap);                  // cc
+    tot += put(fields, nfields, i++, 4 * n);                     // labels
+    tot += put(fields, nfields, i++, 4 * n);                     // best
+    tot += put(fields, nfields, i++, 4 * kcap);                  // counts
+    tot += put(fields, nfields, i++, 4 * n);                     // perm
+    tot += put(fields, nfields, i++, 4 * (kcap + 1));            // starts
+    tot += put(fields, nfields, i++, 4 * tiles * kcap);          // tile_hist
+    tot += put(fields, nfields, i++, 4 * (mi > 0 ? mi : 1));     // inertia
+    tot += put(fields, nfields, i++, 4 * kcap);                  // movement
+    tot += put(fields, nfields, i++, 4 * 8);                     // status
+    tot += put(fields, nfields, i++, 4 * ac_pw_plan_len(n));     // plan_n
+    tot += put(fields, nfields, i++, 0);                         // plan_k (reserved)
+    tot += put(fields, nfields, i++, 8 * n);                     // dscratch
+    tot += put(fields, nfields, i++, (dtype == AC_DTYPE_F32 && fast) ? 2 * 3 * n * d : 0);  // planes
+    tot += put(fields, nfields, i++, fast ? 8 * kcap * d : 0);   // csum
+    tot += put(fields, nfields, i++, fast ? 4 * kcap * d : 0);   // cabs
+    tot += put(fields, nfields, i++, fast ? 4 * kcap * d : 0);   // clsb
+    return tot;
+  }
+  if (op == AC_WS_SELECT) {
+    if (!need(4)) return -1;
+    const int64_t gq = dims[0], c = dims[1], topk = dims[2], stride = dims[3];
+    int i = 0;
+    tot += put(fields, nfields, i++, 4 * gq * c);                // scores
+    tot += put(fields, nfields, i++, 8 * gq * topk);             // selected
+    tot += put(fields, nfields, i++, 4 * gq * stride * 2);       // runs
+    tot += put(fields, nfields, i++, 4 * gq);                    // nruns
+    tot += put(fields, nfields, i++, 8 * gq);                    // covered
+    tot += put(fields, nfields, i++, 8);                         // density
+    return tot;
+  }
+  if (op == AC_WS_ATTENTION) {
+    if (!need(6)) return -1;
+    const int64_t L = dims[0], heads = dims[1], gq_max = dims[2], d = dims[4], dtype = dims[5];
+    const int64_t esz = dtype == AC_DTYPE_BF16 ? 2 : 4;
+    const int64_t qp_cap = L + 128 * gq_max;
+    const int64_t item_cap = (L + 127) / 128 + gq_max;
+    int i = 0;
+    tot += put(fields, nfields, i++, heads * qp_cap * d * esz);              // qp
+    tot += put(fields, nfields, i++, 4 * (heads * qp_cap + heads * gq_max)); // qidx (+ pad starts)
+    tot += put(fields, nfields, i++, heads * item_cap * (int64_t)sizeof(ac_attn_item));  // items
+    tot += put(fields, nfields, i++, heads * L * d * esz);                   // kp
+    tot += put(fields, nfields, i++, heads * L * d * esz);                   // vp
+    return tot;
+  }
+  ac_host::set_error("ac_workspace_bytes: unknown op %d", op);
+  return -1;
+}

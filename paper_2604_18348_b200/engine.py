@@ -94,29 +94,39 @@ class Batch:
             raise ParameterError("batch mixes GEMM accumulation orders")
         N, K, D, P = sum(self.ns), sum(self.kcaps), self.D, self.P
         tiles = [(n + TILE - 1) // TILE for n in self.ns]
-        self.xx = torch.empty(N, dtype=F32, device=dev)
-        self.labels = torch.empty(N, dtype=I32, device=dev)
-        self.best = torch.empty(N, dtype=F32, device=dev)
-        self.perm = torch.empty(N, dtype=I32, device=dev)
-        self.dscratch = torch.empty(N, dtype=torch.float64, device=dev)
-        self.centers = torch.empty(K * D, dtype=F32, device=dev)
-        self.cc = torch.empty(K, dtype=F32, device=dev)
-        self.counts = torch.empty(K, dtype=I32, device=dev)
-        self.starts = torch.empty(K + P, dtype=I32, device=dev)
-        self.movement = torch.empty(K, dtype=F32, device=dev)
-        self.tile_hist = torch.empty(max(sum(t * c for t, c in zip(tiles, self.kcaps)), 1),
-                                     dtype=I32, device=dev)
-        self.inertia = torch.zeros(P * self.max_iter, dtype=F32, device=dev)
+        # buffer sizes from the C-ABI's workspace query (ac_workspace_bytes),
+        # summed over the problems: the header is the single source of truth
+        ws = batch_buffer_bytes(self.ns, self.kcaps, D, self.dtype, self.max_iter)
+
+        def buf(name, dtype, fill=None):
+            n = ws[name] // torch.empty((), dtype=dtype).element_size()
+            if n == 0:
+                return None
+            if fill is None:
+                return torch.empty(n, dtype=dtype, device=dev)
+            return torch.full((n,), fill, dtype=dtype, device=dev)
+
+        self.xx = buf("xx", F32)
+        self.labels = buf("labels", I32)
+        self.best = buf("best", F32)
+        self.perm = buf("perm", I32)
+        self.dscratch = buf("dscratch", torch.float64)
+        self.centers = buf("centers", F32)
+        self.cc = buf("cc", F32)
+        self.counts = buf("counts", I32)
+        self.starts = buf("starts", I32)
+        self.movement = buf("movement", F32)
+        self.tile_hist = buf("tile_hist", I32) if ws["tile_hist"] else torch.empty(
+            1, dtype=I32, device=dev)
+        self.inertia = buf("inertia", F32, 0.0)
         # f32 points: exact bf16 hi/mid/lo planes for the tensor-core assign
         # (written by ac_lloyd_prepare), [3][n][D] per problem
-        self.planes = (torch.empty(3 * N * D, dtype=torch.bfloat16, device=dev)
-                       if self.dtype == L.DTYPE_F32 and D in (64, 128) else None)
+        self.planes = buf("planes", torch.bfloat16)
         # split-chain centroid update workspaces (zeroed; the kernels re-zero)
-        fast = D in (64, 128)
-        self.csum = torch.zeros(K * D, dtype=torch.float64, device=dev) if fast else None
-        self.cabs = torch.zeros(K * D, dtype=F32, device=dev) if fast else None
-        self.clsb = torch.full((K * D,), 0x7F800000, dtype=I32, device=dev) if fast else None
-        self.status = torch.zeros(P * L.STATUS_WORDS, dtype=I32, device=dev)
+        self.csum = buf("csum", torch.float64, 0.0)
+        self.cabs = buf("cabs", F32, 0.0)
+        self.clsb = buf("clsb", I32, 0x7F800000)
+        self.status = buf("status", I32, 0)
         desc = np.zeros(P, dtype=L.PROBLEM_DTYPE)
         self.n_off, self.k_off, self.t_off = [], [], []
         no = ko = to = 0
@@ -227,6 +237,16 @@ class Batch:
     def sort(self):
         """tile histograms must be current (written by assign)."""
         L.call("ac_repair_sort", *self.args(), -1, L.ASSIGN_ALL, L.stream_ptr())
+
+
+def batch_buffer_bytes(ns, kcaps, d: int, dtype: int, max_iter: int) -> dict:
+    """Byte size of every flat buffer of a batch: the per-problem sizes of
+    ac_workspace_bytes(AC_WS_CLUSTER) summed over the problems."""
+    tot: dict[str, int] = {}
+    for n, k in zip(ns, kcaps):
+        for name, b in L.workspace_bytes(L.WS_CLUSTER, n, k, d, dtype, max(max_iter, 1)).items():
+            tot[name] = tot.get(name, 0) + b
+    return tot
 
 
 def _group_by_order(ns, ks, D):
@@ -679,6 +699,54 @@ def sparse_attention_heads(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                    kp.data_ptr(), vp.data_ptr(), dt, da, Ln, H, items.data_ptr(), H * item_cap,
                    runs.data_ptr(), scale, out.data_ptr(), odt, L.stream_ptr())
     return out[..., :D] if da != D else out
+
+
+def dense_attention_1h(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out_dtype=F32,
+                       impl: str = "auto") -> torch.Tensor:
+    """full_attention (reference.py:25-45) for one head with any Lq, Lk >= 1
+    and value width Dv: q [Lq, D], k [Lk, D], v [Lk, Dv] -> [Lq, Dv].
+
+    One query cluster of Lq rows in identity order attends over the single
+    key run [0, Lk).  q and k are zero-padded to a common kernel width
+    (zero columns add nothing to q·k; the softmax scale stays 1/sqrt(D)),
+    v likewise (padded output columns are dropped)."""
+    Lq, D = int(q.shape[0]), int(q.shape[1])
+    Lk, Dv = int(k.shape[0]), int(v.shape[1])
+    dev = L.device()
+    da = _attn_dim(max(D, Dv))
+    dt = L.dtype_code(q)
+    qa, ka, va = (_pad_dim(t, da) for t in (q, k, v))
+    item_rows = 128 if impl == "simt" else int(L.lib().ac_attention_item_rows(dt, da))
+    ident = torch.arange(Lq, dtype=I32, device=dev)
+    counts = torch.tensor([Lq], dtype=I32, device=dev)
+    starts = torch.tensor([0, Lq], dtype=I32, device=dev)
+    labels = torch.zeros(Lq, dtype=I32, device=dev)
+    gq = torch.ones(1, dtype=I32, device=dev)
+    nruns = torch.ones((1, 1), dtype=I32, device=dev)
+    runs = torch.tensor([[[[0, Lk]]]], dtype=I32, device=dev)
+    qp_cap = Lq + TILE
+    item_cap = (Lq + TILE - 1) // TILE + 1
+    qp = torch.empty((qp_cap, da), dtype=q.dtype, device=dev)
+    qidx = torch.empty(qp_cap + 1, dtype=I32, device=dev)
+    items = torch.empty(item_cap * L.ITEM_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    L.call("ac_build_q_layout", qa.data_ptr(), dt, da, Lq, 1, ident.data_ptr(), starts.data_ptr(),
+           counts.data_ptr(), labels.data_ptr(), gq.data_ptr(), 1, nruns.data_ptr(), 1,
+           qp.data_ptr(), qidx.data_ptr(), qp_cap, items.data_ptr(), item_cap, item_rows,
+           L.stream_ptr())
+    out = torch.empty((Lq, da), dtype=out_dtype, device=dev)
+    odt = L.dtype_code(out) if out_dtype != F32 else L.DTYPE_F32
+    scale = float(1.0 / math.sqrt(D))
+    # one head: the head stride L of the K/V tensors is Lk; the output rows
+    # are addressed through qidx (tokens < Lq)
+    if impl == "simt":
+        L.call("ac_sparse_attention_simt", qp.data_ptr(), qidx.data_ptr(), ka.data_ptr(),
+               va.data_ptr(), dt, da, Lk, items.data_ptr(), item_cap, runs.data_ptr(), scale,
+               out.data_ptr(), odt, L.stream_ptr())
+    else:
+        L.call("ac_sparse_attention", qp.data_ptr(), qp_cap, qidx.data_ptr(), ka.data_ptr(),
+               va.data_ptr(), dt, da, Lk, 1, items.data_ptr(), item_cap, runs.data_ptr(), scale,
+               out.data_ptr(), odt, L.stream_ptr())
+    return out[:, :Dv] if da != Dv else out
 
 
 def dense_attention_heads(q, k, v, out_dtype=F32, impl: str = "auto") -> torch.Tensor:

@@ -19,8 +19,9 @@ from .clustering import ClusterModel, import_model
 from .errors import DimensionError, ParameterError
 from .tensorops import to_device, to_host
 
-__all__ = ["ClusterEnvelope", "SelectionResult", "build_envelopes", "tensor_quest",
-           "tensor_quest_clamped_centers", "mean_center_scores", "select_topk_clusters"]
+__all__ = ["ClusterEnvelope", "SelectionResult", "build_envelopes", "quest_scalar",
+           "quest_scores_loop", "tensor_quest", "tensor_quest_clamped_centers",
+           "mean_center_scores", "select_topk_clusters"]
 
 DEFAULT_TOPK = 64
 
@@ -86,6 +87,38 @@ def _scores(q_reps, a, b, scorer: str):
     sels, _, _ = E.select_batch([q.contiguous()], [ta.contiguous()], [tb.contiguous()], [dummy], [1],
                                 scorer)
     return to_host(sels[0].scores, host)
+
+
+def _quest_pairs(q_reps, env: ClusterEnvelope, clusters=None):
+    q, host = to_device(q_reps, keep_bf16=False)
+    mx, _ = to_device(env.max_vec, keep_bf16=False)
+    mn, _ = to_device(env.min_vec, keep_bf16=False)
+    if q.ndim == 1:
+        q = q.reshape(1, -1)
+    if q.shape[1] != mx.shape[1]:
+        raise DimensionError(f"query dim {q.shape[1]} != envelope dim {mx.shape[1]}")
+    if clusters is not None:
+        mx, mn = mx[clusters:clusters + 1], mn[clusters:clusters + 1]
+    q, mx, mn = q.contiguous(), mx.contiguous(), mn.contiguous()
+    out = torch.empty((q.shape[0], mx.shape[0]), dtype=torch.float32, device=q.device)
+    L.call("ac_quest_pairs", q.data_ptr(), int(q.shape[0]), int(q.shape[1]), mx.data_ptr(),
+           mn.data_ptr(), int(mx.shape[0]), out.data_ptr(), L.stream_ptr())
+    return out, host
+
+
+def quest_scalar(q_row, env: ClusterEnvelope, c: int) -> float:
+    """Upper bound on q·k over the members of cluster ``c`` in the scalar
+    form sum_t max(q_t·max_ct, q_t·min_ct) (quest.py:74-77), on the device."""
+    q, _ = to_device(q_row, keep_bf16=False)
+    out, _ = _quest_pairs(q.reshape(1, -1), env, clusters=int(c))
+    return float(out[0, 0].item())
+
+
+def quest_scores_loop(q_reps, env: ClusterEnvelope):
+    """Scalar-form scores of every (query rep, cluster) pair (quest.py:80-91):
+    the same per-pair bound as ``quest_scalar``, one device thread per pair."""
+    out, host = _quest_pairs(q_reps, env)
+    return to_host(out, host)
 
 
 def tensor_quest(q_reps, env: ClusterEnvelope):

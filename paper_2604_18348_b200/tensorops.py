@@ -17,7 +17,8 @@ from . import _lib as L
 from . import engine as E
 from .errors import DimensionError
 
-__all__ = ["as_f32", "l2_normalize_rows", "NormalizedRows", "to_device", "to_host"]
+__all__ = ["as_f32", "matmul", "row_softmax", "l2_normalize_rows", "NormalizedRows",
+           "to_device", "to_host"]
 
 DEGENERATE_NORM = 1e-12
 
@@ -48,6 +49,40 @@ def to_host(t: torch.Tensor | None, host: bool):
     if t.dtype == torch.bfloat16:
         t = t.float()
     return t.cpu().numpy()
+
+
+def matmul(a, b):
+    """f32 matrix product a @ b (tensorops.py:29-37) on the device, in the
+    accumulation order the reference's OpenBLAS call uses for the shape."""
+    ta, host = to_device(a, keep_bf16=False)
+    tb, _ = to_device(b, keep_bf16=False)
+    if ta.ndim != 2 or tb.ndim != 2:
+        raise DimensionError(f"matmul expects 2-D operands, got {tuple(ta.shape)} and "
+                             f"{tuple(tb.shape)}")
+    if ta.shape[1] != tb.shape[0]:
+        raise DimensionError(f"matmul inner dimensions differ: {tuple(ta.shape)} x "
+                             f"{tuple(tb.shape)}")
+    m, kd, n = int(ta.shape[0]), int(ta.shape[1]), int(tb.shape[1])
+    out = torch.zeros((m, n), dtype=torch.float32, device=ta.device)
+    if kd > 0:
+        order = L.gemm_order(m, n, kd)
+        for r0 in range(0, m, 65535):  # grid.y limit per launch
+            r1 = min(m, r0 + 65535)
+            L.call("ac_matmul", ta[r0:r1].data_ptr(), r1 - r0, kd, tb.data_ptr(), n,
+                   out[r0:r1].data_ptr(), order, L.stream_ptr())
+    return to_host(out, host)
+
+
+def row_softmax(s, scale: float = 1.0):
+    """Stable softmax over the last axis of ``scale * s`` (tensorops.py:40-51)."""
+    t, host = to_device(s, keep_bf16=False)
+    t = t.contiguous()
+    out = torch.empty_like(t)
+    cols = int(t.shape[-1]) if t.ndim else 1
+    rows = t.numel() // cols if cols else 0
+    L.call("ac_row_softmax", t.data_ptr(), rows, cols, float(scale), out.data_ptr(),
+           L.stream_ptr())
+    return to_host(out, host)
 
 
 class NormalizedRows(NamedTuple):

@@ -113,3 +113,38 @@ def test_error_codes_map_to_reference_exceptions():
         L.check(L.AC_ERR_CONTRACT)
     with pytest.raises(RuntimeError):
         L.check(L.AC_ERR_CUDA)
+
+
+@pytest.mark.parametrize("n,k,d,dtype", [(70000, 100, 64, L.DTYPE_BF16), (4096, 65, 64, L.DTYPE_F32),
+                                         (300, 7, 17, L.DTYPE_F32), (1, 1, 128, L.DTYPE_BF16)])
+def test_workspace_bytes_cluster(n, k, d, dtype):
+    """ac_workspace_bytes(AC_WS_CLUSTER) sizes every buffer of one
+    ac_cluster_problem; the Python Batch allocates exactly the sum."""
+    from paper_2604_18348_b200.engine import batch_buffer_bytes
+    f = L.workspace_bytes(L.WS_CLUSTER, n, k, d, dtype, 25)
+    fast = d in (64, 128)
+    assert f["xx"] == f["labels"] == f["best"] == f["perm"] == 4 * n
+    assert f["centers"] == 4 * k * d and f["starts"] == 4 * (k + 1)
+    assert f["tile_hist"] == 4 * ((n + 127) // 128) * k
+    assert f["dscratch"] == 8 * n and f["status"] == 32 and f["inertia"] == 100
+    assert f["plan_n"] == 4 * int(L.lib().ac_pw_plan_len(n))
+    assert f["planes"] == (6 * n * d if (fast and dtype == L.DTYPE_F32) else 0)
+    assert f["csum"] == (8 * k * d if fast else 0)
+    tot = batch_buffer_bytes([n, n], [k, k], d, dtype, 25)
+    assert all(tot[x] == 2 * f[x] for x in f)
+
+
+def test_workspace_bytes_select_attention_and_errors():
+    s = L.workspace_bytes(L.WS_SELECT, 65, 100, 25, 25)
+    assert s == {"scores": 4 * 65 * 100, "selected": 8 * 65 * 25, "runs": 4 * 65 * 25 * 2,
+                 "nruns": 4 * 65, "covered": 8 * 65, "density": 8}
+    a = L.workspace_bytes(L.WS_ATTENTION, 70000, 30, 65, 25, 64, L.DTYPE_BF16)
+    qp_cap = 70000 + 128 * 65
+    assert a["qp"] == 30 * qp_cap * 64 * 2
+    assert a["items"] == 30 * ((70000 + 127) // 128 + 65) * L.ITEM_DTYPE.itemsize
+    assert a["kp"] == a["vp"] == 30 * 70000 * 64 * 2
+    from paper_2604_18348_b200.errors import ParameterError
+    with pytest.raises(ParameterError):
+        L.workspace_bytes(7, 1, 2, 3)
+    with pytest.raises(ParameterError):
+        L.workspace_bytes(L.WS_CLUSTER, 10, 2)

@@ -1,0 +1,77 @@
+"""The reference package's own test suite (pkg/tests, 171 tests) run in
+place against this package through module aliases (tests/conformance/
+refalias.py): every public function the tests touch runs on the B200
+library, and the reference's unmodified harness drives it as a caller.
+
+The suite is located at /root/reference/pkg/tests (this container) or
+baseline/_ref_tests (staged by tools/stage_reference_tests.sh, git-ignored,
+travels to the GPU box like baseline/_ref); skipped when neither exists.
+
+Tests that cannot pass by design are listed in EXPECTED_FAIL with the
+reason; every other reference test must pass.
+"""
+
+from __future__ import annotations
+
+import os
+import re
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+
+# reference test id -> why it cannot pass here
+EXPECTED_FAIL = {
+    # matplotlib is not installed in this image (the figures module is out of scope)
+    "tests/test_harness.py::TestRunExperiment::test_figures_rendered": "matplotlib absent",
+    "tests/test_harness.py::TestCli::test_run_renders_figures_by_default": "matplotlib absent",
+}
+
+
+def _suite() -> Path | None:
+    for cand in (Path("/root/reference/pkg/tests"), ROOT / "baseline" / "_ref_tests"):
+        if (cand / "test_pipeline.py").exists():
+            return cand
+    return None
+
+
+def test_reference_suite_against_package(tmp_path):
+    suite = _suite()
+    if suite is None:
+        pytest.skip("reference test suite not available (run tools/stage_reference_tests.sh)")
+    junit = tmp_path / "junit.xml"
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([str(ROOT / "tests" / "conformance"), str(ROOT),
+                                         env.get("PYTHONPATH", "")])
+    cmd = [sys.executable, "-m", "pytest", "-p", "refalias", "-p", "no:cacheprovider", "-q",
+           "-o", "addopts=", "--rootdir", str(suite.parent), f"--junitxml={junit}", str(suite)]
+    res = subprocess.run(cmd, cwd=str(tmp_path), env=env, capture_output=True, text=True,
+                         timeout=1500)
+    print(res.stdout[-6000:])
+    print(res.stderr[-3000:])
+    import xml.etree.ElementTree as ET
+    failed, passed = [], 0
+    for case in ET.parse(junit).getroot().iter("testcase"):
+        cls = case.get("classname", "")
+        # classname "tests.test_x.TestY" -> tests/test_x.py::TestY::name
+        parts = cls.split(".")
+        mod_idx = next(i for i, p in enumerate(parts) if p.startswith("test_"))
+        tid = "tests/" + parts[mod_idx] + ".py"
+        if parts[mod_idx + 1:]:
+            tid += "::" + "::".join(parts[mod_idx + 1:])
+        tid += "::" + re.sub(r"\[.*", "", case.get("name", ""))
+        bad = case.find("failure") is not None or case.find("error") is not None
+        if bad:
+            failed.append(tid)
+        elif case.find("skipped") is None:
+            passed += 1
+    unexpected = sorted(set(failed) - set(EXPECTED_FAIL))
+    print(f"reference suite: {passed} passed, {len(failed)} failed "
+          f"({len(failed) - len(unexpected)} expected)")
+    assert not unexpected, unexpected
+    assert passed >= 160
