@@ -214,7 +214,7 @@ int ac_assign_ordered(const ac_cluster_problem* probs, int nprob, int dtype,
                       int order, const ac_cluster_problem* host_probs,
                       void* stream);
 
-/* assignment kernel selection (process-wide): AUTO = tensor cores when the
+/* assignment kernel selection (per calling thread): AUTO = tensor cores when the
  * batch is eligible, EXACT = always the all-FFMA sequential-chain kernel
  * (the parity reference), TC = tensor cores or AC_ERR_PARAM.               */
 #define AC_ASSIGN_MODE_AUTO 0
@@ -222,7 +222,7 @@ int ac_assign_ordered(const ac_cluster_problem* probs, int nprob, int dtype,
 #define AC_ASSIGN_MODE_TC 2
 int ac_set_assign_mode(int mode);
 int ac_get_assign_mode(void);
-/* centroid-update kernel selection (process-wide): 0 = split-chain sums with
+/* centroid-update kernel selection (per calling thread): 0 = split-chain sums with
  * an exact f32 enclosure test (member-order chain per dimension only when
  * the enclosure straddles a rounding boundary) when the batch has csum/cabs
  * workspaces, 1 = always the member-order f64 chains (the default: its
@@ -310,7 +310,9 @@ typedef struct ac_attn_item {
  * ac_row_softmax out = softmax(scale * s) over the last axis (row-max
  *                subtraction), rows x cols f32
  * ac_quest_pairs out[g, c] = sum_t max(q[g,t]*emax[c,t], q[g,t]*emin[c,t]) in
- *                numpy's pairwise order (the scalar Quest bound, quest_scalar) */
+ *                numpy's pairwise order (the scalar Quest bound, quest_scalar),
+ *                evaluated one pair at a time like the reference's
+ *                quest_scores_loop timing baseline (quest.py:80-91)          */
 int ac_matmul(const float* a, int64_t m, int k, const float* b, int64_t n, float* out,
               int order, void* stream);
 int ac_row_softmax(const float* s, int64_t rows, int64_t cols, float scale, float* out,

@@ -185,7 +185,14 @@ def _davies_bouldin(x: torch.Tensor, cen: torch.Tensor, lab: torch.Tensor, cnt: 
     if c < 2:
         return 0.0
     dist = torch.linalg.norm(x - cen[lab], dim=1)
-    s = torch.zeros(c, dtype=torch.float64, device=x.device).index_add_(0, lab, dist) / cnt
+    # per-cluster sums without atomics (run-to-run deterministic, like the
+    # reference's np.add.at): stable member order, f64 scan, segment ends
+    order = torch.sort(lab, stable=True).indices
+    csum = torch.cumsum(dist[order], 0)
+    ends = torch.cumsum(torch.bincount(lab, minlength=c), 0)
+    tot = csum[(ends - 1).clamp(min=0)]
+    tot = torch.where(ends > 0, tot, torch.zeros_like(tot))
+    s = torch.diff(tot, prepend=torch.zeros(1, dtype=tot.dtype, device=tot.device)) / cnt
     m = torch.cdist(cen, cen)
     ratio = (s[:, None] + s[None, :]) / torch.where(m > 0, m, torch.full_like(m, math.inf))
     ratio.fill_diagonal_(-math.inf)

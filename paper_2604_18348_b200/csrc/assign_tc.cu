@@ -634,16 +634,11 @@ bool assign_tc_eligible(const ac_cluster_problem* host_probs, int nprob, int dty
 int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* host_probs,
                      int nprob, int dtype, int d, int c_lo, int flags, cudaStream_t st) {
   using namespace ac::asg;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    for (const void* f : {(const void*)k_assign_tc<64, 2>, (const void*)k_assign_tc<128, 2>,
-                          (const void*)k_assign_tc<64, 3>, (const void*)k_assign_tc<128, 3>}) {
-      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
-      if (e != cudaSuccess) return check_cuda(e, "k_assign_tc smem");
-    }
+  const int sms = ac_host::sm_count();
+  for (const void* f : {(const void*)k_assign_tc<64, 2>, (const void*)k_assign_tc<128, 2>,
+                        (const void*)k_assign_tc<64, 3>, (const void*)k_assign_tc<128, 3>}) {
+    const int rc = ac_host::func_smem(f, SMEM_MAX, "k_assign_tc smem");
+    if (rc) return rc;
   }
   for (int p0 = 0; p0 < nprob; p0 += MAXP) {
     const int np = std::min(MAXP, nprob - p0);

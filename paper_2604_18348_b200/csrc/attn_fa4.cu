@@ -532,13 +532,7 @@ extern "C" int ac_sparse_attention_fa4(const void* q, int64_t q_rows_total, cons
     return rc;
   if ((rc = ac_host::make_map_2d(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (int64_t)heads * L, D, 64, BN)))
     return rc;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute((const void*)k_attn_fa4,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return ac_host::check_cuda(e, "k_attn_fa4 smem");
-    attr = true;
-  }
+  if ((rc = ac_host::func_smem((const void*)k_attn_fa4, SMEM, "k_attn_fa4 smem"))) return rc;
   const float scale_log2 = scale * 1.4426950408889634f;
   k_attn_fa4<<<nitems, THREADS, SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(
       mq, mk, mv, qidx, L, items, runs, scale_log2, out, out_dtype);

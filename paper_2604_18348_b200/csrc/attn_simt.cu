@@ -264,9 +264,8 @@ int launch_simt(const void* q, const int32_t* qidx, const void* k, const void* v
                 int64_t L, const ac_attn_item* items, int nitems, const int32_t* runs, float scale,
                 void* out, int out_dtype, cudaStream_t st) {
   const size_t smem = simt_smem<D>();
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_attn_simt<D>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return ac_host::check_cuda(e, "k_attn_simt smem");
+  const int rc = ac_host::func_smem((const void*)k_attn_simt<D>, (int)smem, "k_attn_simt smem");
+  if (rc) return rc;
   k_attn_simt<D><<<nitems, 256, smem, st>>>(q, qidx, k, v, dtype, L, items, runs, scale, out, out_dtype);
   AC_CHECK_LAUNCH("k_attn_simt");
   return AC_OK;

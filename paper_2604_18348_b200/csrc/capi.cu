@@ -3,7 +3,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "tc_common.cuh"
@@ -24,6 +27,38 @@ void set_error(const char* fmt, ...) {
 int check_cuda(cudaError_t e, const char* what) {
   set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
   return AC_ERR_CUDA;
+}
+
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, int> g_attr_done;  // (kernel, device) -> bytes set
+std::mutex g_sm_mu;
+int g_sms[64] = {0};
+}  // namespace
+
+int func_smem(const void* fn, int bytes, const char* what) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return check_cuda(e, what);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  auto it = g_attr_done.find({fn, dev});
+  if (it != g_attr_done.end() && it->second >= bytes) return AC_OK;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return check_cuda(e, what);
+  g_attr_done[{fn, dev}] = bytes;
+  return AC_OK;
+}
+
+int sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  std::lock_guard<std::mutex> lk(g_sm_mu);
+  if (!g_sms[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev] = n > 0 ? n : 148;
+  }
+  return g_sms[dev];
 }
 }  // namespace ac_host
 

@@ -1677,16 +1677,15 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
 }  // namespace ac_host
 
 namespace {
-int g_assign_mode = AC_ASSIGN_MODE_AUTO;
+// kernel-selection modes are per calling thread (a process may drive several
+// GPUs or serve concurrent callers from several threads)
+thread_local int g_assign_mode = AC_ASSIGN_MODE_AUTO;
 // 0: split-chain update when eligible, 1: member-order chains (default)
-int g_update_mode = getenv("AC_UPDATE_MODE") ? atoi(getenv("AC_UPDATE_MODE")) : 1;
+thread_local int g_update_mode = getenv("AC_UPDATE_MODE") ? atoi(getenv("AC_UPDATE_MODE")) : 1;
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int set_smem(const void* fn, size_t bytes) {
-  if (bytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return ac_host::check_cuda(e, "cudaFuncSetAttribute");
-  }
+  if (bytes > 48 * 1024) return ac_host::func_smem(fn, (int)bytes, "cudaFuncSetAttribute");
   return AC_OK;
 }
 size_t plan_vals_bytes(int64_t n, size_t elem) {

@@ -109,6 +109,13 @@ AC_DEV void argmax_merge(float& bd, int64_t& bi, float od, int64_t oi) {
 namespace ac_host {
 void set_error(const char* fmt, ...);
 int check_cuda(cudaError_t e, const char* what);
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the CURRENT device,
+// raised only when a call needs more than already set for (kernel, device) --
+// thread-safe, so one process may drive
+// several GPUs from several threads.
+int func_smem(const void* fn, int bytes, const char* what);
+// multiprocessor count of the current device (cached per device)
+int sm_count();
 }  // namespace ac_host
 
 #define AC_CHECK_LAUNCH(what)                                                   \

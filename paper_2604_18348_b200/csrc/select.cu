@@ -163,9 +163,8 @@ extern "C" int ac_select(const ac_select_problem* probs, int nprob, int d, int s
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t smem = sizeof(float) * ((size_t)d + max_c) + sizeof(int) * 2 * (size_t)max_c;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void*)k_select,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return ac_host::check_cuda(e, "k_select smem");
+    const int rc = ac_host::func_smem((const void*)k_select, (int)smem, "k_select smem");
+    if (rc) return rc;
   }
   k_select<<<dim3(max_gq, nprob), 256, smem, st>>>(probs, d, scorer);
   k_density<<<nprob, 256, 0, st>>>(probs);

@@ -106,21 +106,30 @@ k_row_softmax(const float* __restrict__ s, float* __restrict__ out, int64_t cols
   for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) orow[c] = __fdiv_rn(orow[c], sum);
 }
 
-// quest_scalar (quest.py:74-77): float(np.maximum(q*max_c, q*min_c).sum()),
-// the products in f32 and the length-d sum in numpy's pairwise order.
-__global__ void k_quest_pairs(const float* __restrict__ q, int gq, int d,
-                              const float* __restrict__ emax, const float* __restrict__ emin,
-                              int c, float* __restrict__ out) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)gq * c) return;
-  const int g = (int)(e / c), cl = (int)(e - (int64_t)g * c);
+AC_DEV void quest_pair(const float* __restrict__ q, int d, const float* __restrict__ emax,
+                       const float* __restrict__ emin, int g, int cl, float* out) {
   const float* qr = q + (int64_t)g * d;
   const float* mx = emax + (int64_t)cl * d;
   const float* mn = emin + (int64_t)cl * d;
   auto get = [&](int t) {
     return np_maximum(__fmul_rn(qr[t], mx[t]), __fmul_rn(qr[t], mn[t]));
   };
-  out[e] = pw_sum<float>(get, d);
+  *out = pw_sum<float>(get, d);
+}
+
+// quest_scalar (quest.py:74-77): float(np.maximum(q*max_c, q*min_c).sum()),
+// the products in f32 and the length-d sum in numpy's pairwise order.
+// quest_scores_loop (quest.py:80-91) is the reference's deliberately
+// pair-at-a-time timing baseline for tensor_quest, so this kernel runs as ONE
+// thread walking the pairs in (g, c) order -- the scalar form, not a second
+// parallel scorer (the parallel scorer is k_select's matmul form).
+__global__ void k_quest_pairs(const float* __restrict__ q, int gq, int d,
+                              const float* __restrict__ emax, const float* __restrict__ emin,
+                              int c, float* __restrict__ out) {
+  for (int64_t e = 0; e < (int64_t)gq * c; ++e) {
+    const int g = (int)(e / c), cl = (int)(e - (int64_t)g * c);
+    quest_pair(q, d, emax, emin, g, cl, out + e);
+  }
 }
 
 }  // namespace ac
@@ -171,7 +180,7 @@ extern "C" int ac_quest_pairs(const float* q, int gq, int d, const float* emax, 
   const int64_t total = (int64_t)gq * c;
   if (total == 0) return AC_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  k_quest_pairs<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(q, gq, d, emax, emin, c, out);
+  k_quest_pairs<<<1, 1, 0, st>>>(q, gq, d, emax, emin, c, out);
   AC_CHECK_LAUNCH("ac_quest_pairs");
   return AC_OK;
 }

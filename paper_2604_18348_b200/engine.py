@@ -77,7 +77,7 @@ class Batch:
     share D, dtype and the reference's GEMM accumulation order."""
 
     def __init__(self, xs: list[torch.Tensor], ks: list[int], max_iter: int,
-                 kcaps: list[int] | None = None):
+                 kcaps: list[int] | None = None, planes: torch.Tensor | None = None):
         if not xs:
             raise ParameterError("empty batch")
         dev = L.device()
@@ -121,7 +121,12 @@ class Batch:
         self.inertia = buf("inertia", F32, 0.0)
         # f32 points: exact bf16 hi/mid/lo planes for the tensor-core assign
         # (written by ac_lloyd_prepare), [3][n][D] per problem
-        self.planes = buf("planes", torch.bfloat16)
+        if planes is not None and ws["planes"]:  # caller-provided (shared workspace)
+            if planes.numel() * planes.element_size() < ws["planes"]:
+                raise ParameterError("planes workspace too small")
+            self.planes = planes
+        else:
+            self.planes = buf("planes", torch.bfloat16)
         # split-chain centroid update workspaces (zeroed; the kernels re-zero)
         self.csum = buf("csum", torch.float64, 0.0)
         self.cabs = buf("cabs", F32, 0.0)
@@ -397,9 +402,26 @@ class _RunningAssign:
         self.nc = 0
         self.orders: list[int] = []
 
+    def _grow(self, need: int):
+        """Re-home the running state into a batch with room for ``need``
+        centres (a custom stage_schedule can exceed the default bound)."""
+        old = self.batch
+        cap = max(need, 2 * old.kcaps[0])
+        nb = Batch([self.k], [1], old.max_iter, kcaps=[cap])
+        nb.xx.copy_(old.xx)
+        if self.nc:
+            nb.centers_of(0, self.nc).copy_(old.centers_of(0, self.nc))
+            nb.labels.copy_(old.labels)
+            nb.best.copy_(old.best)
+        nb.desc[0]["k"] = old.desc[0]["k"]
+        nb.desc[0]["order"] = old.desc[0]["order"]
+        self.batch = nb
+
     def add(self, centers: torch.Tensor):
-        b = self.batch
         m = centers.shape[0]
+        if self.nc + m > self.batch.kcaps[0]:
+            self._grow(self.nc + m)
+        b = self.batch
         b.centers_of(0, self.nc + m)[self.nc:].copy_(centers)
         new_nc = self.nc + m
         order = L.gemm_order(b.ns[0], new_nc, b.D)
@@ -438,7 +460,10 @@ def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0:
         n = int(ks[h].shape[0])
         st.append(dict(n=n, pool=torch.arange(n, dtype=torch.int64, device=dev), size=n,
                        nc=0, rnd=0, flag=False, iters=0, mse=[], blocks=[],
-                       run=_RunningAssign(ks[h], n_max + m0, max_iter)))
+                       # centres accumulate while nc < n_max, each round adding
+                       # m_t <= max(STAGE_FLOOR=8, m0) (clustering.py:272-286);
+                       # a custom schedule may exceed it (then the batch grows)
+                       run=_RunningAssign(ks[h], n_max - 1 + max(8, m0), max_iter)))
     live = [h for h in range(H) if taus[h] > 0.0]
     for h in range(H):
         if taus[h] <= 0.0:

@@ -88,9 +88,11 @@ def read_npy(path) -> np.ndarray:
     path = Path(path)
     shape, off = npy_header(path, path.stat().st_size)
     out = np.empty(shape, dtype=np.float32)
+    if out.size == 0:  # e.g. shape (0, 64): nothing to read
+        return out
     with open(path, "rb") as f:
         f.seek(off)
-        f.readinto(memoryview(out).cast("B"))
+        f.readinto(out.reshape(-1).view(np.uint8))
     return out
 
 
@@ -183,8 +185,10 @@ def load_layer(directory, step: int, layer: int, dtype=None, device="cuda"):
         for h, hd in enumerate(heads):
             p = hd / f"{name}.npy"
             _, off = npy_header(p)
+            if buf[h].size == 0:
+                continue
             with open(p, "rb") as f:
                 f.seek(off)
-                f.readinto(memoryview(buf[h]).cast("B"))
+                f.readinto(buf[h].reshape(-1).view(np.uint8))
         out.append(stage.to(device, non_blocking=True).to(dtype))
     return tuple(out)

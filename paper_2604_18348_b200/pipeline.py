@@ -416,6 +416,8 @@ class LayerSession:
         self.last = None
         self.graph = graph
         self.steady = None  # SteadyStep (CUDA graph) once the warm step is fixed
+        self._plan = None   # step-0 plan made by plan() ahead of step 0
+        self.workspace_pool = None  # dict shared by the layers of a StackSession
 
     # carried state (pipeline.py:85-90); lives in the steady step's batches
     @property
@@ -453,11 +455,43 @@ class LayerSession:
             return float("nan")
         return float(self.last[2].selections[0].density.item())
 
-    def step(self, Q, K, V, host_out=None):
+    def _seeds(self, H: int) -> list:
+        return [self.seed + 7919 * self.layer + self.head_offset + h for h in range(H)]
+
+    def plan(self, Q, K):
+        """Step-0 planning of this layer's heads without attention
+        (run_denoise_steps' planning pass, pipeline.py:310-324): returns the
+        per-head key-clustering MSE (f64, device) and flag_full list.  The
+        caller then fixes the layer policy (``set_mode``) -- across layers for
+        the quota, across ranks for sharded heads -- and step 0 reuses the plan."""
+        if self.t != 0:
+            raise ContractError("plan() is the step-0 planning pass")
+        dev = L.device()
+        Q, K = (x if (isinstance(x, torch.Tensor) and x.device.type == "cuda")
+                else torch.as_tensor(x).to(dev) for x in (Q, K))
+        H = int(Q.shape[0])
+        if H == 0:
+            self._plan = "empty"
+            return torch.zeros(0, dtype=torch.float64, device=dev), []
+        run = LayerRunner(self.params, None, self.attn_impl)
+        plan = run.plan(Q, K, self._seeds(H))
+        self._plan = plan
+        mse = E.mse_batch([K[h] for h in range(H)], plan.key_models)
+        return mse, [bool(m.flag_full) for m in plan.key_models]
+
+    def set_mode(self, mode: str):
+        """Fix the layer policy decided from plan() (``full`` or ``sparse``)."""
+        if mode not in ("full", "sparse"):
+            raise ParameterError(f"mode must be 'full' or 'sparse', got {mode!r}")
+        self.mode = mode
+
+    def step(self, Q, K, V, host_out=None, async_out: bool = False):
         """One denoising step of the layer.  With host (pinned) inputs the
         result is written to ``host_out`` (a pinned host tensor of the output
         shape, e.g. preallocated by a serving loop) or to a fresh pinned
-        tensor; the host copy is asynchronous on the current stream."""
+        tensor, and is ready when the call returns (like the reference's
+        numpy result); ``async_out=True`` returns as soon as the device->host
+        copy is enqueued on the current stream (synchronise before reading)."""
         host = not (isinstance(Q, torch.Tensor) and Q.device.type == "cuda")
         dev = L.device()
         if host:
@@ -467,16 +501,29 @@ class LayerSession:
                     and host_out is not None and all(x.is_pinned() for x in (Q, K, V, host_out))):
                 # steady state from pinned buffers: copies inside the graph
                 self.t += 1
-                return st.step_host(Q, K, V, host_out)
+                res = st.step_host(Q, K, V, host_out)
+                if not async_out:
+                    torch.cuda.current_stream().synchronize()
+                return res
             Q, K, V = (x.to(dev, non_blocking=True) for x in (Q, K, V))
         odt = self.out_dtype or (torch.bfloat16 if Q.dtype == torch.bfloat16 else torch.float32)
         run = LayerRunner(self.params, odt, self.attn_impl)
         H = Q.shape[0]
+        if H == 0:  # a rank without heads of this layer (head sharding)
+            if self.t == 0 and self._plan is None:
+                self.mode = "full" if self.reduce_flag(False) else "sparse"
+            self.t += 1
+            return torch.empty(tuple(Q.shape), dtype=odt, device=Q.device)
         if self.t == 0:
-            seeds = [self.seed + 7919 * self.layer + self.head_offset + h for h in range(H)]
-            plan = run.plan(Q, K, seeds)
-            flagged = self.reduce_flag(any(m.flag_full for m in plan.key_models))
-            self.mode = "full" if flagged else "sparse"
+            if self._plan is not None:  # planned ahead; policy fixed by set_mode
+                plan = self._plan
+                self._plan = None
+                if self.mode is None:
+                    raise ContractError("plan() was called but set_mode() was not")
+            else:
+                plan = run.plan(Q, K, self._seeds(H))
+                flagged = self.reduce_flag(any(m.flag_full for m in plan.key_models))
+                self.mode = "full" if flagged else "sparse"
             if self.mode == "sparse":
                 so = run.sparse(Q, K, V, plan.q_models, plan.reps, plan.key_models,
                                 self.params.topk)
@@ -491,13 +538,21 @@ class LayerSession:
         elif self.mode == "full":
             with phase("attention_dense"):
                 out = run.dense(Q, K, V)
-        elif self.graph and self.attn_impl == "auto" and self.params.scorer == "quest":
+        elif (self.graph and self.attn_impl == "auto" and self.params.scorer == "quest"
+              and int(Q.shape[2]) in E.ATTN_DIMS):
             from .steady import SteadyStep
             if self.steady is None or self.steady.Q.shape != Q.shape or self.steady.dtype != Q.dtype:
+                from .steady import Workspace
                 kc, qc = self.key_centers, self.query_centers
                 self.steady = None
+                ws = None
+                if self.workspace_pool is not None:
+                    key = (H, int(Q.shape[1]), int(Q.shape[2]), Q.dtype, int(qc[0].shape[0]), odt)
+                    ws = self.workspace_pool.get(key)
+                    if ws is None:
+                        ws = self.workspace_pool[key] = Workspace(*key)
                 self.steady = SteadyStep(H, Q.shape[1], Q.shape[2], Q.dtype, self.params, kc, qc,
-                                         odt)
+                                         odt, workspace=ws)
                 self.last = None
             with phase("steady_step"):
                 out = self.steady.step(Q, K, V)
@@ -515,5 +570,7 @@ class LayerSession:
             res = host_out if host_out is not None else torch.empty(out.shape, dtype=out.dtype,
                                                                      pin_memory=True)
             res.copy_(out, non_blocking=True)
+            if not async_out:
+                torch.cuda.current_stream().synchronize()
             return res
         return out

@@ -31,6 +31,34 @@ F32 = torch.float32
 I32 = torch.int32
 
 
+class Workspace:
+    """The large per-step buffers of a warm step ([H, L, D]-sized: static
+    inputs, normalised queries and their bf16 planes, permuted K/V, the
+    padded query layout, output).  A layer stack shares one workspace across
+    its layers' graphs (layers run one after another), so a 40-layer stack
+    holds one layer's worth of these instead of forty."""
+
+    def __init__(self, H: int, Ln: int, D: int, dtype: torch.dtype, gq: int, out_dtype=None):
+        dev = L.device()
+        odt = out_dtype or (torch.bfloat16 if dtype == torch.bfloat16 else F32)
+        self.key = (H, Ln, D, dtype, gq, odt)
+        self.Q = torch.empty((H, Ln, D), dtype=dtype, device=dev)
+        self.K = torch.empty((H, Ln, D), dtype=dtype, device=dev)
+        self.V = torch.empty((H, Ln, D), dtype=dtype, device=dev)
+        self.qn = torch.empty((H, Ln, D), dtype=F32, device=dev)
+        self.qdeg = torch.empty(H * Ln, dtype=torch.uint8, device=dev)
+        self.planes = (torch.empty(3 * H * Ln * D, dtype=torch.bfloat16, device=dev)
+                       if D in (64, 128) else None)
+        self.kp, self.vp = ws.kp, ws.vp
+        self.qp_cap = Ln + E.TILE * gq
+        self.item_cap = (Ln + E.TILE - 1) // E.TILE + gq
+        self.qp = torch.empty((H * self.qp_cap, D), dtype=dtype, device=dev)
+        self.qidx = torch.empty(H * self.qp_cap + H * gq, dtype=I32, device=dev)
+        self.items = torch.empty(H * self.item_cap * L.ITEM_DTYPE.itemsize, dtype=torch.uint8,
+                                 device=dev)
+        self.out = torch.empty((H, Ln, D), dtype=odt, device=dev)
+
+
 class SteadyStep:
     """Graph-captured warm step for H heads of [L, D] (bf16 or f32).
 
@@ -39,14 +67,21 @@ class SteadyStep:
     (valid until the next call)."""
 
     def __init__(self, H: int, Ln: int, D: int, dtype: torch.dtype, params, key_centers: list,
-                 query_centers: list, out_dtype=None, use_graph: bool = True, split: int = 2):
+                 query_centers: list, out_dtype=None, use_graph: bool = True, split: int = 2,
+                 workspace: Workspace | None = None):
         dev = L.device()
         self.H, self.L, self.D, self.dtype = H, Ln, D, dtype
         self.p = params
         self.out_dtype = out_dtype or (torch.bfloat16 if dtype == torch.bfloat16 else F32)
-        self.Q = torch.empty((H, Ln, D), dtype=dtype, device=dev)
-        self.K = torch.empty((H, Ln, D), dtype=dtype, device=dev)
-        self.V = torch.empty((H, Ln, D), dtype=dtype, device=dev)
+        gq_set = {int(c.shape[0]) for c in query_centers}
+        if len(gq_set) != 1:
+            raise ValueError("steady step expects one query-cluster count for all heads")
+        gq0 = next(iter(gq_set))
+        ws = workspace or Workspace(H, Ln, D, dtype, gq0, self.out_dtype)
+        if ws.key != (H, Ln, D, dtype, gq0, self.out_dtype):
+            raise ValueError("workspace shape does not match the step")
+        self.ws = ws
+        self.Q, self.K, self.V = ws.Q, ws.K, ws.V
         p = params
         # ---- key clustering (warm Lloyd, in place across steps) ----
         self.kb = E.Batch([self.K[h] for h in range(H)], [int(c.shape[0]) for c in key_centers],
@@ -54,13 +89,10 @@ class SteadyStep:
         for h, c in enumerate(key_centers):
             self.kb.centers_of(h).copy_(c.to(F32))
         # ---- query clustering on the normalised queries ----
-        self.qn = torch.empty((H, Ln, D), dtype=F32, device=dev)
-        self.qdeg = torch.empty(H * Ln, dtype=torch.uint8, device=dev)
-        gq = {int(c.shape[0]) for c in query_centers}
-        if len(gq) != 1:
-            raise ValueError("steady step expects one query-cluster count for all heads")
-        self.gq = gq.pop()
-        self.qb = E.Batch([self.qn[h] for h in range(H)], [self.gq] * H, p.max_iter)
+        self.qn, self.qdeg = ws.qn, ws.qdeg
+        self.gq = gq0
+        self.qb = E.Batch([self.qn[h] for h in range(H)], [self.gq] * H, p.max_iter,
+                          planes=ws.planes)
         for h, c in enumerate(query_centers):
             self.qb.centers_of(h).copy_(c.to(F32))
         self.qmodels = [self.qb.model(h) for h in range(H)]
@@ -118,21 +150,16 @@ class SteadyStep:
         if da != D:
             raise ValueError("graph-captured step needs head_dim in (16, 32, 64, 128)")
         self.dt = L.dtype_code(self.Q)
-        self.kp = torch.empty_like(self.K)
-        self.vp = torch.empty_like(self.V)
+        self.kp, self.vp = ws.kp, ws.vp
         self.kperm = self.kb.perm.view(H, Ln)
         self.qperm = self.qb.perm.view(H, Ln)
         self.qlab = self.qb.labels.view(H, Ln)
         self.qcounts = self.qb.counts.view(H, self.gq)
         self.qstarts = self.qb.starts.view(H, self.gq + 1)
         self.gq_t = torch.full((H,), self.gq, dtype=I32, device=dev)
-        self.qp_cap = Ln + E.TILE * self.gq
-        self.item_cap = (Ln + E.TILE - 1) // E.TILE + self.gq
+        self.qp_cap, self.item_cap = ws.qp_cap, ws.item_cap
         self.item_rows = int(L.lib().ac_attention_item_rows(self.dt, D))
-        self.qp = torch.empty((H * self.qp_cap, D), dtype=dtype, device=dev)
-        self.qidx = torch.empty(H * self.qp_cap + H * self.gq, dtype=I32, device=dev)
-        self.items = torch.empty(H * self.item_cap * L.ITEM_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-        self.out = torch.empty((H, Ln, D), dtype=self.out_dtype, device=dev)
+        self.qp, self.qidx, self.items, self.out = ws.qp, ws.qidx, ws.items, ws.out
         self.odt = L.dtype_code(self.out) if self.out_dtype != F32 else L.DTYPE_F32
         self.scale = float(1.0 / math.sqrt(D))
         self.graph = None

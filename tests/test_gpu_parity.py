@@ -293,3 +293,23 @@ def test_compactness_matches_scalar_loops(gpu):
     z = np.tile(np.array([[1.0, 1.0]], np.float32), (4, 1))
     rz = gpu.compactness([z], [gpu.kmeans(z, 1, seed=0)])
     assert rz.mse_layer == 0.0 and math.isinf(rz.comp)
+
+
+@pytest.mark.parametrize("m0,nmax,sched", [(1, 10, None), (3, 5, None), (4, 40, "grow")])
+def test_multi_stage_capacity_edges(gpu, oracle, m0, nmax, sched):
+    """Accumulated centres can reach n_max - 1 + max(8, m0) before the budget
+    check trips (clustering.py:282-290), and a custom stage_schedule may ask
+    for more than m0 per round; both must match the oracle."""
+    spec = LayerSpec(kind="dispersed", gaussian_components=8, component_sigma=0.5,
+                     component_separation=20.0)
+    q, k, v = gen_synthetic(spec, 600, 16, 1, 1, 5)[0][0]
+    schedule = (lambda t, remaining, total: 4 + 9 * t) if sched == "grow" else None
+    s0 = oracle.kmeans(k, m0, 2)
+    tau = oracle.compute_tau(k, s0) * 0.5
+    ma = gpu.multi_stage_cluster_keys(k, tau, n_max=nmax, m0=m0, seed=2, stage0=s0,
+                                      stage_schedule=schedule)
+    mb = oracle.multi_stage(k, tau, n_max=nmax, m0=m0, seed=2, stage0=s0, stage_schedule=schedule)
+    assert ma.flag_full == mb.flag_full and ma.stage_count == mb.stage_count
+    assert np.array_equal(ma.assignments, mb.assignments)
+    assert np.array_equal(ma.centers, mb.centers)
+    assert ma.stage_mse == mb.stage_mse

@@ -130,3 +130,14 @@ def test_load_layer_drives_the_layer_step(gpu, tmp_path):
     o1 = gpu.LayerSession(p, out_dtype=torch.float32).step(Q, K, V).clone()
     o2 = gpu.LayerSession(p, out_dtype=torch.float32).step(*ref).clone()
     assert torch.equal(o1, o2)
+
+
+def test_zero_element_arrays_round_trip(tmp_path):
+    """Valid zero-element arrays (e.g. shape (0, 64)) read back as empty arrays."""
+    from paper_2604_18348_b200.npyio import read_npy, write_npy
+    for shape in [(0, 64), (0,), (3, 0)]:
+        p = tmp_path / f"z{len(shape)}_{shape[0]}.npy"
+        write_npy(p, np.zeros(shape, np.float32))
+        out = read_npy(p)
+        assert out.shape == shape and out.dtype == np.float32
+        assert np.load(p).shape == shape
