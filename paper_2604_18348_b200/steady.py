@@ -49,7 +49,8 @@ class Workspace:
         self.qdeg = torch.empty(H * Ln, dtype=torch.uint8, device=dev)
         self.planes = (torch.empty(3 * H * Ln * D, dtype=torch.bfloat16, device=dev)
                        if D in (64, 128) else None)
-        self.kp, self.vp = ws.kp, ws.vp
+        self.kp = torch.empty_like(self.K)
+        self.vp = torch.empty_like(self.V)
         self.qp_cap = Ln + E.TILE * gq
         self.item_cap = (Ln + E.TILE - 1) // E.TILE + gq
         self.qp = torch.empty((H * self.qp_cap, D), dtype=dtype, device=dev)
