@@ -24,7 +24,7 @@ import numpy as np
 import pytest
 import torch
 
-from workload.synthetic import CRIT7_SPEC, LayerSpec, gen_synthetic
+from workload.synthetic import CRIT7_SPEC, LayerSpec, gen_outlier_steps, gen_synthetic
 
 pytestmark = pytest.mark.gpu
 
@@ -41,7 +41,10 @@ def rel_l2(ref, x):
 def _inputs(spec, L, D, heads, seeds, dtype):
     """[t] -> (Q, K, V) [H, L, D] torch (CPU) in ``dtype``; plus the f32
     values the oracle sees (bf16-rounded when dtype is bf16)."""
-    per = [gen_synthetic(spec, L, D, 1, T_STEPS, s) for s in seeds[:heads]]
+    if isinstance(spec, tuple):  # ("outlier", frac_tail): the adaptive-count workload
+        per = [gen_outlier_steps(L, D, T_STEPS, s, spec[1], drift_sigma=DRIFT) for s in seeds[:heads]]
+    else:
+        per = [gen_synthetic(spec, L, D, 1, T_STEPS, s) for s in seeds[:heads]]
     dev, ora = [], []
     for t in range(T_STEPS):
         trip = [torch.from_numpy(np.stack([per[h][t][0][j] for h in range(heads)])).to(dtype)
@@ -114,7 +117,7 @@ def _run(P, O, spec, L, D, heads, seeds, dtype, q_clusters, topk, tol, label):
             assert np.array_equal(sess.key_centers[h].cpu().numpy(), states[h].key_centers), where
             assert np.array_equal(sess.query_centers[h].cpu().numpy(),
                                   states[h].query_centers), where
-    return report
+    return report, sess
 
 
 def test_c1_crit7_f32(gpu, oracle):
@@ -146,3 +149,14 @@ def test_c4_head_bf16(gpu, oracle):
     """C4: one HunyuanVideo head, L=118800, D=128, bf16."""
     spec = dataclasses.replace(CRIT7_SPEC, drift_sigma=DRIFT)
     _run(gpu, oracle, spec, 118800, 128, 1, [1000], torch.bfloat16, 65, 25, 1e-2, "C4")
+
+
+def test_c3_outlier_heads_adaptive_counts(gpu, oracle):
+    """C3-sized heads of the outlier-cloud workload (bench C3 spec mix): the
+    multi-stage planner runs tens of rounds and the key-cluster count adapts
+    (> m0 = 100); everything still bit-exact against the oracle."""
+    _, sess = _run(gpu, oracle, ("outlier", 0.002), 32760, 128, 2, [1001, 1002], torch.bfloat16,
+                   65, 25, 1e-2, "C3-outlier")
+    counts = [int(c.shape[0]) for c in sess.key_centers]
+    print("key clusters", counts)
+    assert all(c > 100 for c in counts)

@@ -17,7 +17,7 @@ for h in range(cfg["heads"]):
         ins[t].append(s[t][0])
 dev = [[torch.stack([torch.from_numpy(x[j]) for x in ins[t]]).bfloat16().cuda() for j in range(3)]
        for t in range(2)]
-sess = P.LayerSession(bench._params(P), out_dtype=torch.bfloat16)
+sess = P.LayerSession(bench._params(P, cfg), out_dtype=torch.bfloat16)
 for i in range(3):
     sess.step(*dev[i % 2])
 torch.cuda.synchronize()

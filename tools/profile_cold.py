@@ -18,9 +18,9 @@ ins = []
 for h in range(cfg["heads"]):
     ins.append(bench.gen_head(cfg, h)[0][0])
 dev = [torch.stack([torch.from_numpy(x[j]) for x in ins]).to(tdt).cuda() for j in range(3)]
-P.LayerSession(bench._params(P), out_dtype=tdt).step(*dev)
+P.LayerSession(bench._params(P, cfg), out_dtype=tdt).step(*dev)
 torch.cuda.synchronize()
-sess = P.LayerSession(bench._params(P), out_dtype=tdt)
+sess = P.LayerSession(bench._params(P, cfg), out_dtype=tdt)
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
     t0 = time.perf_counter()
     sess.step(*dev)

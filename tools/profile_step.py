@@ -32,7 +32,7 @@ dev = []
 for t in range(2):
     dev.append([torch.stack([torch.from_numpy(x[j]) for x in ins[t]]).to(tdt).cuda()
                 for j in range(3)])
-sess = P.LayerSession(bench._params(P), out_dtype=tdt)
+sess = P.LayerSession(bench._params(P, cfg), out_dtype=tdt)
 sess.step(*dev[0])
 for i in range(args.warmup):
     sess.step(*dev[(i + 1) % 2])
