@@ -84,7 +84,7 @@ CONFIGS = {
     "c4": dict(name="C4 HunyuanVideo layer", heads=24, seq=118800, dim=128, dtype="bf16",
                specs=["crit7"], topk=25, layers=1, quota=0.0),
     "c5": dict(name="C5 Wan-2.1-14B 40-layer stack (per-layer spec cycle, quota 0.15)", heads=40,
-               seq=75600, dim=128, dtype="bf16", specs=["crit7", "mid", "outlier1"], topk=25,
+               seq=75600, dim=128, dtype="bf16", specs=["crit7", "mid", "wide"], topk=25,
                layers=40, quota=0.15, pool=4),
 }
 

@@ -51,7 +51,7 @@ namespace asg {
 using namespace ac::tc;
 
 constexpr int BM = 128;     // rows per tile (== kAsgBM: shared tiling with the sort kernels)
-constexpr int NBMAX = 128;  // centres per problem per launch (k - c_lo)
+constexpr int NBMAX = kAsgTcChunk;  // centres per problem per launch (k - c_lo)
 constexpr int ATOM = BM * 128;  // one SW128 K-atom (64 bf16 columns) of a 128-row tile
 constexpr int MAXP = 32;    // problems per launch (tensor maps travel as kernel params)
 constexpr int W_TMA = 0, W_MMA = 1, W_EPI0 = 2;
@@ -61,6 +61,7 @@ constexpr int CF_STRIDE = 64 + 4;       // f32 centre rows (D = 64), padded agai
 constexpr int QCAP = 64;                // per-warp queue of extra (row, centre) fix-up candidates
 constexpr int SMEM_MAX = 227 * 1024;
 constexpr float kPadE = 3.0e38f;        // e of the padding columns (never a candidate)
+constexpr int kNoHist = kAsgNoHist;     // internal flag: skip the per-tile label histogram
 
 // Shared-memory layout, sized per launch from the largest centre count
 // (cap = max round16(k - c_lo)):
@@ -85,6 +86,7 @@ struct Params {
   int nprob;
   int dtype;
   int c_lo;
+  int c_hi;   // centres [c_lo, min(k, c_hi)) of each problem (chunked assignment)
   int flags;
   int f32_terms;  // split products for f32 points: 3 (default) or 6
   Layout lay;
@@ -293,7 +295,11 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
       t = seg_end;
       continue;
     }
-    const int k = P.k, c_lo = prm.c_lo, nb = k - c_lo;
+    const int k = P.k, c_lo = prm.c_lo, nb = min(k, prm.c_hi) - c_lo;
+    if (nb < 1) {  // no centre of this problem in this chunk
+      t = seg_end;
+      continue;
+    }
     const int nbp = max(16, (nb + 15) & ~15);
     const int64_t n = P.n;
     const int ptile0 = prm.tile0[p];
@@ -564,7 +570,7 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
           P.labels[row] = label;
           P.best[row] = best;
         }
-        if (!(prm.flags & AC_ASSIGN_MERGE)) {
+        if (!(prm.flags & (AC_ASSIGN_MERGE | kNoHist))) {
           named_sync(1 + wg, 128);
           for (int c = r; c < k; c += 128) hist[c] = 0;
           named_sync(1 + wg, 128);
@@ -601,30 +607,35 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
 // ---------------------------------------------------------------------------
 namespace ac_host {
 
-static int tc_cap(const ac_cluster_problem* host_probs, int nprob, int c_lo) {
+static int tc_cap(const ac_cluster_problem* host_probs, int nprob, int c_lo, int c_hi) {
   int cap = 16;
-  for (int j = 0; j < nprob; ++j) cap = std::max(cap, (host_probs[j].k - c_lo + 15) & ~15);
+  for (int j = 0; j < nprob; ++j)
+    cap = std::max(cap, (std::min(host_probs[j].k, c_hi) - c_lo + 15) & ~15);
   return cap;
 }
 
 // Can the tensor-core kernel take this batch?  (D = 64 or 128, general-path
-// accumulation order, <= 128 centres past c_lo, 16-byte aligned rows, and
-// a shared-memory layout with at least one x stage.)
+// accumulation order, <= 128 centres in [c_lo, c_hi), 16-byte aligned rows,
+// and a shared-memory layout with at least one x stage.)
 bool assign_tc_eligible(const ac_cluster_problem* host_probs, int nprob, int dtype, int d,
-                        int c_lo, int order) {
+                        int c_lo, int order, int c_hi) {
   if (!host_probs || order != AC_ORDER_SEQ || (d != 64 && d != 128)) return false;
   if (dtype != AC_DTYPE_F32 && dtype != AC_DTYPE_BF16) return false;
+  bool any = false;
   for (int p = 0; p < nprob; ++p) {
     const ac_cluster_problem& P = host_probs[p];
-    if (P.k - c_lo < 1 || P.k - c_lo > ac::asg::NBMAX) return false;
+    const int nb = std::min(P.k, c_hi) - c_lo;
+    if (nb > ac::asg::NBMAX) return false;
+    any |= nb >= 1;
     if ((reinterpret_cast<uintptr_t>(P.x) & 15) || (reinterpret_cast<uintptr_t>(P.centers) & 15))
       return false;
     // f32 points are read as their exact bf16 planes (written by ac_lloyd_prepare)
     if (dtype == AC_DTYPE_F32 && (!P.planes || (reinterpret_cast<uintptr_t>(P.planes) & 15)))
       return false;
   }
+  if (!any) return false;
   for (int p0 = 0; p0 < nprob; p0 += ac::asg::MAXP) {
-    const int cap = tc_cap(host_probs + p0, std::min(ac::asg::MAXP, nprob - p0), c_lo);
+    const int cap = tc_cap(host_probs + p0, std::min(ac::asg::MAXP, nprob - p0), c_lo, c_hi);
     if (ac::asg::make_layout(dtype, d, cap, 1, ac::asg::f32_terms_env()).smem > ac::asg::SMEM_MAX)
       return false;
   }
@@ -632,7 +643,7 @@ bool assign_tc_eligible(const ac_cluster_problem* host_probs, int nprob, int dty
 }
 
 int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* host_probs,
-                     int nprob, int dtype, int d, int c_lo, int flags, cudaStream_t st) {
+                     int nprob, int dtype, int d, int c_lo, int flags, cudaStream_t st, int c_hi) {
   using namespace ac::asg;
   const int sms = ac_host::sm_count();
   for (const void* f : {(const void*)k_assign_tc<64, 2>, (const void*)k_assign_tc<128, 2>,
@@ -644,7 +655,7 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     const int np = std::min(MAXP, nprob - p0);
     Params prm;
     memset(&prm, 0, sizeof(prm));
-    const int cap = tc_cap(host_probs + p0, np, c_lo);
+    const int cap = tc_cap(host_probs + p0, np, c_lo, c_hi);
     int xs = 4;
     prm.f32_terms = f32_terms_env();
     while (xs > 1 && make_layout(dtype, d, cap, xs, prm.f32_terms).smem > SMEM_MAX) --xs;
@@ -656,6 +667,7 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     prm.nprob = np;
     prm.dtype = dtype;
     prm.c_lo = c_lo;
+    prm.c_hi = c_hi;
     prm.flags = flags;
     prm.tile0[0] = 0;
     for (int j = 0; j < np; ++j) {

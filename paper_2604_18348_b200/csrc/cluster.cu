@@ -1671,9 +1671,10 @@ using namespace ac;
 
 namespace ac_host {
 bool assign_tc_eligible(const ac_cluster_problem* host_probs, int nprob, int dtype, int d,
-                        int c_lo, int order);
+                        int c_lo, int order, int c_hi = INT_MAX);
 int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* host_probs,
-                     int nprob, int dtype, int d, int c_lo, int flags, cudaStream_t st);
+                     int nprob, int dtype, int d, int c_lo, int flags, cudaStream_t st,
+                     int c_hi = INT_MAX);
 }  // namespace ac_host
 
 namespace {
@@ -1801,7 +1802,17 @@ static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
   const unsigned tiles = (unsigned)((max_n + kAsgBM - 1) / kAsgBM);
   const int mode = g_assign_mode;
   const bool tc_ok = ac_host::assign_tc_eligible(host_probs, nprob, dtype, d, c_lo, order);
-  if (mode == AC_ASSIGN_MODE_TC && !tc_ok) {
+  // more than 128 centres: tensor-core passes over 128-centre chunks
+  bool chunk_ok = !tc_ok && mode != AC_ASSIGN_MODE_EXACT && c_lo == 0 &&
+                  !(flags & AC_ASSIGN_MERGE) && max_k <= 4096 &&
+                  ac_host::assign_tc_eligible(host_probs, nprob, dtype, d, 0, order, ac::kAsgTcChunk);
+  for (int c0 = ac::kAsgTcChunk; c0 < max_k && chunk_ok; c0 += ac::kAsgTcChunk) {
+    bool reached = false;  // a chunk no problem reaches is fine
+    for (int p = 0; p < nprob; ++p) reached |= host_probs[p].k > c0;
+    chunk_ok = !reached ||
+               ac_host::assign_tc_eligible(host_probs, nprob, dtype, d, c0, order, c0 + ac::kAsgTcChunk);
+  }
+  if (mode == AC_ASSIGN_MODE_TC && !tc_ok && !chunk_ok) {
     ac_host::set_error("assign: tensor-core path forced but the batch is not eligible "
                        "(needs D=64/128, general order, k-c_lo<=128, host descriptors)");
     return AC_ERR_PARAM;
@@ -1810,6 +1821,32 @@ static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
     if (!cc_valid) k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
     AC_CHECK_LAUNCH("k_center_sqnorm");
     return ac_host::assign_tc_launch(probs, host_probs, nprob, dtype, d, c_lo, flags, st);
+  }
+  // the first chunk with exact distances, the rest merged with strict '<'
+  // (earlier chunks win ties: the first-index argmin over the whole set),
+  // then the tile histograms of the final labels
+  {
+    const bool ok = chunk_ok;
+    if (ok) {
+      if (!cc_valid) k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, 0);
+      AC_CHECK_LAUNCH("k_center_sqnorm");
+      const int base = (flags & ~AC_ASSIGN_LABELS_ONLY) | ac::kAsgNoHist;
+      for (int c0 = 0; c0 < max_k; c0 += ac::kAsgTcChunk) {
+        bool any = false;
+        for (int p = 0; p < nprob; ++p) any |= host_probs[p].k > c0;
+        if (!any) break;
+        const int rc = ac_host::assign_tc_launch(probs, host_probs, nprob, dtype, d, c0,
+                                                 base | (c0 ? AC_ASSIGN_MERGE : 0), st,
+                                                 c0 + ac::kAsgTcChunk);
+        if (rc) return rc;
+      }
+      const size_t hsm = sizeof(int) * (size_t)(max_k + 4);
+      int rc = set_smem((const void*)k_tile_hist, hsm);
+      if (rc) return rc;
+      k_tile_hist<<<dim3(tiles, nprob), kAsgBM, hsm, st>>>(probs, max_k);
+      AC_CHECK_LAUNCH("k_tile_hist");
+      return AC_OK;
+    }
   }
   if (order == AC_ORDER_SEQ) {
     const size_t smem = assign_smem_bytes(d, max_k);

@@ -18,6 +18,10 @@
 namespace ac {
 
 constexpr int kWarp = 32;
+// tensor-core assignment (assign_tc.cu): centres per pass, and the internal
+// flag that skips its per-tile label histogram (chunked passes rebuild it)
+constexpr int kAsgTcChunk = 128;
+constexpr int kAsgNoHist = 1 << 8;
 
 // ---------------------------------------------------------------------------
 // element loads: the clustering path reads keys either as f32 or as bf16

@@ -190,3 +190,35 @@ def test_labels_only_lloyd_with_empty_cluster_repair(gpu, oracle, dtype):
     ref = oracle.lloyd(x.float().numpy(), init.numpy(), 25, 1e-4)
     assert np.array_equal(l1, ref.assignments)
     assert np.array_equal(c1, ref.centers)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("ks", [(129,), (200,), (300, 100), (100, 257, 140)])
+def test_tc_assign_chunked_over_128_centres(gpu, dtype, ks, d):
+    """k > 128: 128-centre tensor-core passes merged with strict '<' (first
+    index wins across chunks) + rebuilt tile histograms == the exact kernel."""
+    g = torch.Generator().manual_seed(sum(ks) * 7 + d)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    xs, cs = [], []
+    for j, k in enumerate(ks):
+        n = 4000 + 1500 * j
+        x = (torch.randn(n, d, generator=g) * 20).to(tdt).cuda()
+        c = (x.float().cpu()[torch.randint(0, n, (k,), generator=g)] +
+             torch.randn(k, d, generator=g) * 0.5)
+        c[k // 2] = c[3]  # duplicated centres across chunks: ties -> the lower index
+        xs.append(x)
+        cs.append(c.cuda())
+    _compare(xs, cs)
+
+
+def test_lloyd_with_chunked_assign_matches_oracle(gpu, oracle):
+    """A 200-centre Lloyd run (chunked tensor-core assign) equals the oracle."""
+    rng = np.random.default_rng(11)
+    x = (rng.normal(size=(9000, 64)) * 5).astype(np.float32)
+    init = x[rng.choice(9000, 200, replace=False)] + 0.1
+    a = gpu.warm_start_update(x, init)
+    b = oracle.warm_start(x, init)
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centers, b.centers)
+    assert a.n_iter == b.n_iter
