@@ -26,7 +26,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--extended-lambda",
     "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", "-Xptxas", "-warn-spills",
-]
+] + os.environ.get("AC_NVCC_FLAGS", "").split()  # A/B experiments only (e.g. -DAC_ASG_X_GLOBAL=0)
 # translation unit -> extra flags
 UNITS = {
     "capi.cu": [],

@@ -55,7 +55,7 @@ constexpr int NBMAX = kAsgTcChunk;  // centres per problem per launch (k - c_lo)
 constexpr int ATOM = BM * 128;  // one SW128 K-atom (64 bf16 columns) of a 128-row tile
 constexpr int MAXP = 32;    // problems per launch (tensor maps travel as kernel params)
 constexpr int W_TMA = 0, W_MMA = 1, W_EPI0 = 2;
-constexpr int NWG_MAX = 3;  // epilogue warpgroups (one tile / TMEM accumulator each)
+constexpr int NWG_MAX = 4;  // epilogue warpgroups (one tile / TMEM accumulator each)
 constexpr int threads_for(int nwg) { return 64 + 128 * nwg; }
 constexpr int CF_STRIDE = 64 + 4;       // f32 centre rows (D = 64), padded against bank conflicts
 constexpr int QCAP = 64;                // per-warp queue of extra (row, centre) fix-up candidates
@@ -230,7 +230,7 @@ AC_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // NWG = 2: 320 threads (<= 168 registers); NWG = 3: 448 threads, compiled
 // for 512 (<= 128 registers: 4 warps share an SM sub-partition's 64 KB file)
 template <int DIM, int NWG>
-__global__ void __launch_bounds__(NWG == 2 ? 320 : 512, 1)
+__global__ void __launch_bounds__(NWG == 2 ? 320 : (NWG == 3 ? 512 : 576), 1)
 k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __restrict__ probs) {
   constexpr int THREADS = threads_for(NWG);
   constexpr int KB = DIM / 64;           // SW128 K-atoms per row
@@ -647,7 +647,8 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
   using namespace ac::asg;
   const int sms = ac_host::sm_count();
   for (const void* f : {(const void*)k_assign_tc<64, 2>, (const void*)k_assign_tc<128, 2>,
-                        (const void*)k_assign_tc<64, 3>, (const void*)k_assign_tc<128, 3>}) {
+                        (const void*)k_assign_tc<64, 3>, (const void*)k_assign_tc<128, 3>,
+                        (const void*)k_assign_tc<64, 4>, (const void*)k_assign_tc<128, 4>}) {
     const int rc = ac_host::func_smem(f, SMEM_MAX, "k_assign_tc smem");
     if (rc) return rc;
   }
@@ -686,9 +687,15 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     const int grid = std::min(total, sms);
     // 3 epilogue warpgroups (measured faster than 2 for both dtypes once the
     // f32 MMA runs three split products); AC_ASG_WG=2 selects the 320-thread form
-    static const int env_wg = getenv("AC_ASG_WG") ? atoi(getenv("AC_ASG_WG")) : 3;
-    const int nwg = env_wg == 2 ? 2 : 3;
-    if (nwg == 2) {
+    // epilogue warpgroups: 4 at D = 64 (measured -0.27 ms per C2 step: more
+    // warps hide the epilogue's latency chains), 3 at D = 128 (4 spill there);
+    // AC_ASG_WG overrides
+    static const int env_wg = getenv("AC_ASG_WG") ? atoi(getenv("AC_ASG_WG")) : 0;
+    const int nwg = (env_wg >= 2 && env_wg <= 4) ? env_wg : (d == 64 ? 4 : 3);
+    if (nwg == 4) {
+      if (d == 64) k_assign_tc<64, 4><<<grid, threads_for(4), prm.lay.smem, st>>>(prm, probs + p0);
+      else k_assign_tc<128, 4><<<grid, threads_for(4), prm.lay.smem, st>>>(prm, probs + p0);
+    } else if (nwg == 2) {
       if (d == 64) k_assign_tc<64, 2><<<grid, threads_for(2), prm.lay.smem, st>>>(prm, probs + p0);
       else k_assign_tc<128, 2><<<grid, threads_for(2), prm.lay.smem, st>>>(prm, probs + p0);
     } else {
