@@ -445,11 +445,92 @@ class _RunningAssign:
         return out
 
 
+class _RunningAssignBatch:
+    """The running nearest-centre state of several heads' keys at once (one
+    Batch, one problem per head): each round's centres are appended per
+    head and merged into (best, label) with strict '<' -- earlier centres win
+    ties, exactly argmin over the concatenation (clustering.py:301-302) --
+    in one assignment launch per group of heads that share the merge offset
+    and the GEMM order (all of them in lock-step rounds)."""
+
+    def __init__(self, ks: list[torch.Tensor], kcap: int, max_iter: int):
+        self.ks = ks
+        self.max_iter = max_iter
+        self.batch = Batch(ks, [1] * len(ks), max_iter, kcaps=[kcap] * len(ks))
+        self.batch.prepare()  # ||x||^2 of every key (the centres are set per round)
+        self.nc = [0] * len(ks)
+        self.orders: list[list[int]] = [[] for _ in ks]
+
+    def _grow(self, need: list[int]):
+        old = self.batch
+        caps = [max(n, c) for n, c in zip(need, old.kcaps)]
+        caps = [c if c <= k else max(c, 2 * k) for c, k in zip(caps, old.kcaps)]
+        nb = Batch(self.ks, [1] * len(self.ks), self.max_iter, kcaps=caps)
+        nb.xx.copy_(old.xx)
+        nb.labels.copy_(old.labels)
+        nb.best.copy_(old.best)
+        for p, nc in enumerate(self.nc):
+            if nc:
+                nb.centers_of(p, nc).copy_(old.centers_of(p, nc))
+            nb.desc[p]["k"] = old.desc[p]["k"]
+            nb.desc[p]["order"] = old.desc[p]["order"]
+            nb.ks[p] = old.ks[p]
+        self.batch = nb
+
+    def add(self, heads: list[int], centers: list[torch.Tensor]):
+        b = self.batch
+        need = list(b.kcaps)
+        for p, c in zip(heads, centers):
+            need[p] = self.nc[p] + int(c.shape[0])
+        if any(n > c for n, c in zip(need, b.kcaps)):
+            self._grow(need)
+            b = self.batch
+        groups: dict[tuple, list[int]] = {}
+        for p, c in zip(heads, centers):
+            m = int(c.shape[0])
+            nc = self.nc[p]
+            b.centers_of(p, nc + m)[nc:].copy_(c)
+            order = L.gemm_order(b.ns[p], nc + m, b.D)
+            full = nc == 0 or any(o != order for o in self.orders[p])
+            b.desc[p]["k"] = nc + m
+            b.desc[p]["order"] = order
+            b.ks[p] = nc + m
+            groups.setdefault((0 if full else nc, order), []).append(p)
+            self.orders[p].append(order)
+            self.nc[p] = nc + m
+        b.dev = L.to_device_struct(b.desc)
+        for (c_lo, order), ps in groups.items():
+            host = np.ascontiguousarray(b.desc[ps])
+            dev = b.dev if len(ps) == b.P else L.to_device_struct(host)
+            flags = L.ASSIGN_ALL | (L.ASSIGN_MERGE if c_lo else 0)
+            L.call("ac_assign_ordered", dev.data_ptr(), len(ps), b.dtype, b.D,
+                   max(b.ns[p] for p in ps), max(b.ks[p] for p in ps), int(c_lo), flags, order,
+                   host.ctypes.data, L.stream_ptr())
+
+    def mean_best(self, heads: list[int]) -> torch.Tensor:
+        """f32 mean of the running best distances (nearest_center_mse over the
+        accumulated centres) of ``heads`` -> device [len(heads)]."""
+        b = self.batch
+        out = torch.empty(len(heads), dtype=F32, device=L.device())
+        if len(heads) == b.P and heads == list(range(b.P)):
+            dev = b.dev
+        else:
+            dev = L.to_device_struct(np.ascontiguousarray(b.desc[heads]))
+        L.call("ac_reduce_best", dev.data_ptr(), len(heads), max(b.ns[p] for p in heads), 0,
+               out.data_ptr(), L.stream_ptr())
+        self._keep_mb = dev
+        return out
+
+
 def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0: int,
                       seeds: list[int], max_iter: int, tol: float,
                       stage0: list[DevModel | None], schedule=None) -> list[DevModel]:
-    """multi_stage_cluster_keys (clustering.py:218-320, default schedule) for
-    several keys tensors in lock-step rounds.  Rounds need |U| on the host."""
+    """multi_stage_cluster_keys (clustering.py:218-320) for several keys
+    tensors in lock-step rounds, batched across heads: per round one
+    k-means batch over the heads still splitting, one retire launch, one
+    merged assignment per group of heads and ONE host read (|U| and the
+    stage MSE of every head); the final drop-empty / member sort run once
+    for all heads.  Rounds need |U| on the host (it sizes the next round)."""
     dev = L.device()
     H = len(ks)
     D = int(ks[0].shape[1])
@@ -458,18 +539,16 @@ def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0:
     st = []
     for h in range(H):
         n = int(ks[h].shape[0])
-        st.append(dict(n=n, pool=torch.arange(n, dtype=torch.int64, device=dev), size=n,
-                       nc=0, rnd=0, flag=False, iters=0, mse=[], blocks=[],
-                       # centres accumulate while nc < n_max, each round adding
-                       # m_t <= max(STAGE_FLOOR=8, m0) (clustering.py:272-286);
-                       # a custom schedule may exceed it (then the batch grows)
-                       run=_RunningAssign(ks[h], n_max - 1 + max(8, m0), max_iter)))
+        st.append(dict(n=n, pool=None, size=n, nc=0, rnd=0, flag=False, iters=0, mse=[]))
     live = [h for h in range(H) if taus[h] > 0.0]
+    # centres accumulate while nc < n_max, each round adding m_t <= max(STAGE_FLOOR=8, m0)
+    # (clustering.py:272-286); a custom schedule may exceed it (then the batch grows)
+    run = _RunningAssignBatch(ks, n_max - 1 + max(8, m0), max_iter) if live else None
     for h in range(H):
         if taus[h] <= 0.0:
             base = stage0[h] if stage0[h] is not None else kmeans_batch(
                 [ks[h]], [min(m0, st[h]["n"])], [seeds[h]], max_iter, tol)[0]
-            ra = st[h]["run"]
+            ra = _RunningAssign(ks[h], max(base.k, 1), max_iter)
             ra.add(base.centers)
             base.flag_full = True
             base.stage_count = 1
@@ -514,10 +593,13 @@ def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0:
                 st[h]["model"], st[h]["sub"] = m, subx[h]
         # retire: U = U[dist >= tau] (f32 compare, NEP 50)
         desc = np.zeros(len(todo), dtype=L.PROBLEM_DTYPE)
-        outs, scratch = [], []
+        outs = []
+        scratch = []
         for j, h in enumerate(todo):
             s = st[h]
             m = s["model"]
+            if s["pool"] is None:
+                s["pool"] = torch.arange(s["n"], dtype=torch.int64, device=dev)
             sc = torch.empty(s["size"], dtype=torch.float64, device=dev)
             scratch.append(sc)
             e = desc[j]
@@ -535,47 +617,49 @@ def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0:
         cnt = torch.empty(len(todo), dtype=torch.int64, device=dev)
         L.call("ac_retire", dv.data_ptr(), len(todo), dt, D, max(st[h]["size"] for h in todo),
                tau32.data_ptr(), pin.data_ptr(), pout.data_ptr(), cnt.data_ptr(), L.stream_ptr())
-        mses = []
+        run.add(todo, [st[h]["model"].centers for h in todo])
+        mses = run.mean_best(todo)
         for h in todo:
             s = st[h]
             s["iters"] += s["model"].n_iter()
-            s["run"].add(s["model"].centers)
-            s["blocks"].append(s["model"].k)
             s["nc"] += s["model"].k
-            mses.append(s["run"].mean_best())
-        cnt_h = cnt.cpu().numpy()
-        mse_h = torch.cat(mses).cpu().numpy()
+        host = torch.cat([cnt.double(), mses.double()]).cpu().numpy()  # the round's one sync
         for j, h in enumerate(todo):
             s = st[h]
-            s["pool"] = outs[j][:int(cnt_h[j])]
-            s["size"] = int(cnt_h[j])
-            s["mse"].append(float(mse_h[j]))
+            s["pool"] = outs[j][:int(host[j])]
+            s["size"] = int(host[j])
+            s["mse"].append(float(np.float32(host[len(todo) + j])))
             s["rnd"] += 1
         live = [h for h in live if st[h]["size"] > 0 and not st[h]["flag"]]
         for h in list(live):
             if st[h]["nc"] >= n_max:
                 st[h]["flag"] = True
                 live.remove(h)
-    # final labels = running argmin over every accumulated centre; drop empties
+    # final labels = running argmin over every accumulated centre; drop empty
+    # centres and sort members -- one launch each for every head
     fin = [h for h in range(H) if results[h] is None]
-    for h in fin:
-        s = st[h]
-        b = s["run"].batch
-        newk = torch.empty(1, dtype=I32, device=dev)
-        L.call("ac_drop_empty", b.dev.data_ptr(), 1, D, b.max_n, b.max_k, newk.data_ptr(),
+    if fin:
+        b = run.batch
+        sub = L.to_device_struct(np.ascontiguousarray(b.desc[fin]))
+        newk = torch.empty(len(fin), dtype=I32, device=dev)
+        L.call("ac_drop_empty", sub.data_ptr(), len(fin), D, b.max_n, b.max_k, newk.data_ptr(),
                L.stream_ptr())
-        kk = int(newk.item())
-        b.desc[0]["k"] = kk
-        b.ks = [kk]
+        kk = newk.cpu().numpy()
+        for j, p in enumerate(fin):
+            b.desc[p]["k"] = int(kk[j])
+            b.ks[p] = int(kk[j])
         b.dev = L.to_device_struct(b.desc)
-        L.call("ac_sort_by_label", b.dev.data_ptr(), 1, b.max_n, b.max_k, L.stream_ptr())
-        m = b.model(0)
-        m.flag_full = s["flag"]
-        m.stage_count = s["rnd"]
-        m.stage_mse = s["mse"]
-        m.tau = float(taus[h])
-        m.host_iters = s["iters"]
-        results[h] = m
+        sub = L.to_device_struct(np.ascontiguousarray(b.desc[fin]))
+        L.call("ac_sort_by_label", sub.data_ptr(), len(fin), b.max_n, b.max_k, L.stream_ptr())
+        for h in fin:
+            s = st[h]
+            m = b.model(h)
+            m.flag_full = s["flag"]
+            m.stage_count = s["rnd"]
+            m.stage_mse = s["mse"]
+            m.tau = float(taus[h])
+            m.host_iters = s["iters"]
+            results[h] = m
     return results  # type: ignore[return-value]
 
 
