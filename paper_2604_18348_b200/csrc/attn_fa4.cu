@@ -373,8 +373,8 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
           for (int u = 0; u < 32; u += 8)
 #pragma unroll
             for (int a = 0; a < 4; ++a)
-              mx[a] = fmaxf(mx[a], fmaxf(__uint_as_float(sr[ch][u + 2 * a]),
-                                         __uint_as_float(sr[ch][u + 2 * a + 1])));
+              mx[a] = fmax3(mx[a], __uint_as_float(sr[ch][u + 2 * a]),
+                                         __uint_as_float(sr[ch][u + 2 * a + 1]));
         const float ms = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
 #if !AC_FA4_LATE_WAIT
         // P_t / O_t are free once the previous tile's PV has completed

@@ -278,8 +278,8 @@ k_attn_fa4_d128(const __grid_constant__ CUtensorMap tmq, const __grid_constant__
           for (int u = 0; u < 32; u += 8)
 #pragma unroll
             for (int a = 0; a < 4; ++a)
-              mx[a] = fmaxf(mx[a], fmaxf(__uint_as_float(sr[ch][u + 2 * a]),
-                                         __uint_as_float(sr[ch][u + 2 * a + 1])));
+              mx[a] = fmax3(mx[a], __uint_as_float(sr[ch][u + 2 * a]),
+                                         __uint_as_float(sr[ch][u + 2 * a + 1]));
         const float ms = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
         // PV_t(j-1) has completed (S_t(j) was issued after it): O_t may be
         // rescaled below, before P_t(j) is published.  Lazy: the running max

@@ -187,6 +187,13 @@ AC_DEV void named_sync(int id, int threads) {
 }
 
 }  // namespace tc
+// three-input max (FMNMX3 on sm_100): one instruction per pair in the row max
+AC_DEV float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 }  // namespace ac
 
 // host-side tensor-map encoding (driver entry point; no -lcuda needed)
