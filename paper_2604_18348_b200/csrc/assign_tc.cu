@@ -124,7 +124,7 @@ __host__ __device__ inline Layout make_layout(int dtype, int dim, int cap, int x
   l.off_q = l.off_hist + NWG_MAX * NBMAX * 4;
   l.off_bar = l.off_q + 4 * NWG_MAX * QCAP * 8;
   l.off_misc = l.off_bar + 16 * 8;
-  l.smem = l.off_misc + 64 + 1024;  // + alignment slack
+  l.smem = l.off_misc + 32 + 4 * (MAXP + 1) + 1024;  // + alignment slack
   return l;
 }
 
@@ -281,29 +281,38 @@ k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __rest
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int total = prm.tile0[prm.nprob];
+  // The tiles are split evenly over the CTAs counting only problems with
+  // work in this launch (Lloyd-converged problems and problems without a
+  // centre in this chunk contribute none), so converged heads shorten the
+  // launch instead of idling the CTAs they were statically assigned to.
+  // Every CTA derives the same prefix from the device-side status words.
+  int* s_act0 = reinterpret_cast<int*>(sm + lay.off_misc + 32);  // [MAXP + 1]
+  if (tid < prm.nprob) {  // one thread per problem: the loads run in parallel
+    const ac_cluster_problem& Q = probs[tid];
+    const bool act = ((prm.flags & AC_ASSIGN_ALL) || Q.status[AC_ST_ACTIVE] != 0) &&
+                     min(Q.k, prm.c_hi) - prm.c_lo >= 1;
+    s_act0[tid + 1] = act ? prm.tile0[tid + 1] - prm.tile0[tid] : 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    s_act0[0] = 0;
+    for (int q = 0; q < prm.nprob; ++q) s_act0[q + 1] += s_act0[q];
+  }
+  __syncthreads();
+  const int total = s_act0[prm.nprob];
   const int t_begin = (int)((int64_t)blockIdx.x * total / gridDim.x);
   const int t_end = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
   int g0 = 0;  // CTA-local sequence number of the segment's first tile
   int p = 0;
   for (int t = t_begin; t < t_end;) {
-    while (prm.tile0[p + 1] <= t) ++p;
-    const int seg_end = min(t_end, prm.tile0[p + 1]);
+    while (s_act0[p + 1] <= t) ++p;
+    const int seg_end = min(t_end, s_act0[p + 1]);
     const ac_cluster_problem& P = probs[p];
-    const bool active = (prm.flags & AC_ASSIGN_ALL) || P.status[AC_ST_ACTIVE] != 0;
-    if (!active) {
-      t = seg_end;
-      continue;
-    }
     const int k = P.k, c_lo = prm.c_lo, nb = min(k, prm.c_hi) - c_lo;
-    if (nb < 1) {  // no centre of this problem in this chunk
-      t = seg_end;
-      continue;
-    }
     const int nbp = max(16, (nb + 15) & ~15);
     const int64_t n = P.n;
-    const int ptile0 = prm.tile0[p];
-    const int ntiles_p = prm.tile0[p + 1] - ptile0;
+    const int ptile0 = s_act0[p];                            // virtual (active-only) numbering
+    const int ntiles_p = prm.tile0[p + 1] - prm.tile0[p];    // the problem's real tile count
     const int T = seg_end - t;
 
     // ---- centres of this problem: -2c planes and ||c||^2 split (MMA),

@@ -27,5 +27,10 @@ for name in sys.argv[1:] or ["c2"]:
         sess.step(*dev[i % 2])
     torch.cuda.synchronize()
     print(name, sess.steady.trace())
+    from paper_2604_18348_b200 import _lib as L
+    st = sess.steady
+    ki = st.kb.status.view(st.H, -1)[:, L.ST_NITER].tolist()
+    qi = st.qb.status.view(st.H, -1)[:, L.ST_NITER].tolist()
+    print(name, "key Lloyd iterations per head", ki, "query", qi)
     del sess, dev
     torch.cuda.empty_cache()
