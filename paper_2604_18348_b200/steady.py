@@ -68,7 +68,7 @@ class SteadyStep:
     (valid until the next call)."""
 
     def __init__(self, H: int, Ln: int, D: int, dtype: torch.dtype, params, key_centers: list,
-                 query_centers: list, out_dtype=None, use_graph: bool = True, split: int = 2,
+                 query_centers: list, out_dtype=None, use_graph: bool = True, split: int = 0,
                  workspace: Workspace | None = None):
         dev = L.device()
         self.H, self.L, self.D, self.dtype = H, Ln, D, dtype
@@ -169,6 +169,10 @@ class SteadyStep:
         # and around the clustering (kernel time of the last replay)
         self.ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
         # concurrent clustering chains: head blocks x (keys, queries)
+        # one chain pair for small layers (C3: 12 x 32760 -> 5.59 vs 5.70 ms), two
+        # head blocks for large ones (C2: 25.97 vs 26.36 ms); AC_STEADY_SPLIT overrides
+        if split <= 0:
+            split = 1 if H * Ln <= 1_000_000 else 2
         split = int(os.environ.get("AC_STEADY_SPLIT", split))
         self.split = max(1, min(split, H))
         self.hb = (H + self.split - 1) // self.split
