@@ -189,6 +189,9 @@ class SteadyStep:
         # copied back (D2H stream) while the next chunk computes
         self.out_chunks = max(1, min(H, int(os.environ.get("AC_STEADY_OUT_CHUNKS", "5"))))
         self.d2h = torch.cuda.Stream()
+        self.vstream = torch.cuda.Stream()
+        self.v_in = [torch.cuda.Event() for _ in range(self.out_chunks)]
+        self.v_done = [torch.cuda.Event() for _ in range(self.out_chunks)]
         self.chunk_done = [torch.cuda.Event() for _ in range(self.out_chunks)]
         self.d2h_done = torch.cuda.Event()
         # AC_STEADY_TRACE=1: timing events at phase boundaries (trace())
@@ -261,10 +264,17 @@ class SteadyStep:
             with torch.cuda.stream(ks):
                 kb.lloyd_range(h0, h1, p.max_iter, p.tol, inertia=False)
                 self._mark(f"kchain{i}")
+        nc = self.out_chunks
+        bounds = [(H * c) // nc for c in range(nc + 1)]
         if host is not None:
+            # V per attention chunk, after every Q/K block: a chunk's attention
+            # needs only its own heads' V (permuted by the final key clusters)
             with torch.cuda.stream(self.h2d):
-                self.V.copy_(host[2], non_blocking=True)
-                self.fork_v.record(self.h2d)
+                for c in range(nc):
+                    h0, h1 = bounds[c], bounds[c + 1]
+                    if h1 > h0:
+                        self.V[h0:h1].copy_(host[2][h0:h1], non_blocking=True)
+                    self.v_in[c].record(self.h2d)
         else:
             self.fork_v.record(main)
         esz = self.K.element_size()
@@ -284,10 +294,27 @@ class SteadyStep:
                        self.dt, D, kb.max_k, self.pmax.data_ptr() + h0 * 8, self.pmin.data_ptr() + h0 * 8, s)
                 L.call("ac_permute_rows_heads", self.K.data_ptr() + hoff, self.dt, D,
                        self.kperm[h0].data_ptr(), Ln, h1 - h0, self.kp.data_ptr() + hoff, s)
-                ks.wait_event(self.fork_v)
-                L.call("ac_permute_rows_heads", self.V.data_ptr() + hoff, self.dt, D,
-                       self.kperm[h0].data_ptr(), Ln, h1 - h0, self.vp.data_ptr() + hoff, s)
+                if host is None:
+                    ks.wait_event(self.fork_v)
+                    L.call("ac_permute_rows_heads", self.V.data_ptr() + hoff, self.dt, D,
+                           self.kperm[h0].data_ptr(), Ln, h1 - h0, self.vp.data_ptr() + hoff, s)
                 self.joins[2 * i].record(ks)
+        if host is not None:
+            # V permutes per attention chunk on their own stream, as each
+            # chunk's V arrives (the key clusters are final once the key
+            # chains joined)
+            for i in range(len(blocks)):
+                self.vstream.wait_event(self.joins[2 * i])
+            with torch.cuda.stream(self.vstream):
+                for c in range(nc):
+                    h0, h1 = bounds[c], bounds[c + 1]
+                    self.vstream.wait_event(self.v_in[c])
+                    if h1 > h0:
+                        hoff = h0 * Ln * D * esz
+                        L.call("ac_permute_rows_heads", self.V.data_ptr() + hoff, self.dt, D,
+                               self.kperm[h0].data_ptr(), Ln, h1 - h0, self.vp.data_ptr() + hoff,
+                               L.stream_ptr())
+                    self.v_done[c].record(self.vstream)
         for i in range(2 * len(blocks)):
             main.wait_event(self.joins[i])
         s = L.stream_ptr()
@@ -303,10 +330,9 @@ class SteadyStep:
         if host is None:
             self._attend(0, H)
         else:
-            nc = self.out_chunks
-            bounds = [(H * c) // nc for c in range(nc + 1)]
             for c in range(nc):
                 h0, h1 = bounds[c], bounds[c + 1]
+                main.wait_event(self.v_done[c])
                 if h1 <= h0:
                     continue
                 self._attend(h0, h1)
