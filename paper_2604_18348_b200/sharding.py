@@ -85,9 +85,16 @@ def gather_heads_async(local: torch.Tensor, H: int, group=None) -> _Pending:
                            device=local.device)
         work = dist.all_gather_into_tensor(full, pad, group=group, async_op=True)
         return _Pending(work, full, sizes, H, per)
+    dev = pad.device
+    if pad.is_cuda:  # gloo moves host memory: stage through the host
+        pad = pad.cpu()
     parts = [torch.empty_like(pad) for _ in range(world)]
     work = dist.all_gather(parts, pad, group=group, async_op=True)
-    return _Pending(work, parts, sizes, H, per)
+    pend = _Pending(work, parts, sizes, H, per)
+    if dev.type == "cuda":
+        pend.wait()
+        pend.done = pend.done.to(dev)
+    return pend
 
 
 def gather_heads(local: torch.Tensor, H: int, group=None) -> torch.Tensor:
