@@ -265,8 +265,11 @@ def _group_by_order(ns, ks, D):
 # k-means / Lloyd
 # ---------------------------------------------------------------------------
 def kmeans_batch(xs: list[torch.Tensor], ks: list[int], seeds: list[int], max_iter: int,
-                 tol: float) -> list[DevModel]:
-    """clustering.py:155-167 for every problem (k-means++ then Lloyd)."""
+                 tol: float, inertia: bool = True) -> list[DevModel]:
+    """clustering.py:155-167 for every problem (k-means++ then Lloyd).
+    ``inertia=False``: no inertia_history (callers that never read it -- the
+    streaming sessions and the multi-stage rounds -- get the labels-only
+    assignment, same labels / centres / n_iter)."""
     out: list[DevModel | None] = [None] * len(xs)
     D = int(xs[0].shape[1])
     for idx in _group_by_order([x.shape[0] for x in xs], ks, D):
@@ -289,14 +292,17 @@ def kmeans_batch(xs: list[torch.Tensor], ks: list[int], seeds: list[int], max_it
                                              forced_from=int(stops[j]))
             dd = torch.from_numpy(draws).to(L.device())
             b.kmeanspp(dd, mk)
-        b.lloyd(max_iter, tol)
+        if inertia:
+            b.lloyd(max_iter, tol)
+        else:
+            b.lloyd_range(0, b.P, max_iter, tol, inertia=False)
         for j, i in enumerate(idx):
             out[i] = b.model(j)
     return out  # type: ignore[return-value]
 
 
 def lloyd_batch(xs: list[torch.Tensor], inits: list[torch.Tensor], max_iter: int,
-                tol: float) -> list[DevModel]:
+                tol: float, inertia: bool = True) -> list[DevModel]:
     """clustering.py:119-152 from given initial centres (warm starts)."""
     out: list[DevModel | None] = [None] * len(xs)
     D = int(xs[0].shape[1])
@@ -305,7 +311,10 @@ def lloyd_batch(xs: list[torch.Tensor], inits: list[torch.Tensor], max_iter: int
         b = Batch([xs[i] for i in idx], [ks[i] for i in idx], max_iter)
         for j, i in enumerate(idx):
             b.centers_of(j).copy_(inits[i].to(F32))
-        b.lloyd(max_iter, tol)
+        if inertia:
+            b.lloyd(max_iter, tol)
+        else:
+            b.lloyd_range(0, b.P, max_iter, tol, inertia=False)
         for j, i in enumerate(idx):
             out[i] = b.model(j)
     return out  # type: ignore[return-value]
@@ -342,13 +351,14 @@ def segment_means(xs: list[torch.Tensor], models: list[DevModel]) -> list[torch.
 
 
 def cluster_queries_batch(qs: list[torch.Tensor], num_clusters: list[int], seeds: list[int],
-                          max_iter: int, tol: float, inits: list[torch.Tensor] | None = None):
+                          max_iter: int, tol: float, inits: list[torch.Tensor] | None = None,
+                          inertia: bool = True):
     """clustering.py:182-200: normalise, cluster (cold or warm), representatives."""
     qns = [l2norm(q)[0] for q in qs]
     if inits is None:
-        models = kmeans_batch(qns, num_clusters, seeds, max_iter, tol)
+        models = kmeans_batch(qns, num_clusters, seeds, max_iter, tol, inertia)
     else:
-        models = lloyd_batch(qns, inits, max_iter, tol)
+        models = lloyd_batch(qns, inits, max_iter, tol, inertia)
     reps = segment_means(qns, models)
     return models, reps, qns
 

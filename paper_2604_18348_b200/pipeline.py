@@ -140,10 +140,19 @@ class LayerRunner:
     selection and block-sparse attention.  Heads are independent
     (SPEC.md:242); batching only amortises launches."""
 
-    def __init__(self, params: PipelineParams, out_dtype=torch.float32, attn_impl: str = "auto"):
+    def __init__(self, params: PipelineParams, out_dtype=torch.float32, attn_impl: str = "auto",
+                 inertia: bool = True):
         self.p = params
         self.out_dtype = out_dtype
         self.attn_impl = attn_impl
+        # inertia_history is only exported by the model-returning API
+        # (adacluster_attention, run_denoise_steps); the streaming sessions
+        # skip it in the WARM Lloyd passes (labels-only assignment).  Cold
+        # k-means keeps it: starting from k-means++ seeds, empty clusters are
+        # common and their repair needs the exact distances of every row,
+        # which the labels-only path recomputes in one CTA per problem
+        # (measured: C2 step 0 99 -> 145 ms when cold passes skipped it)
+        self.inertia = inertia
 
     def plan(self, Q: torch.Tensor, K: torch.Tensor, seeds: list[int]) -> LayerPlan:
         """_plan_head (pipeline.py:168-185) for every head."""
@@ -170,10 +179,12 @@ class LayerRunner:
         p = self.p
         H = Q.shape[0]
         with phase("warm_keys"):
-            km = E.lloyd_batch([K[h] for h in range(H)], key_centers, p.max_iter, p.tol)
+            km = E.lloyd_batch([K[h] for h in range(H)], key_centers, p.max_iter, p.tol,
+                               self.inertia)
         with phase("warm_queries"):
             qm, reps, _ = E.cluster_queries_batch([Q[h] for h in range(H)], [0] * H, [0] * H,
-                                                  p.max_iter, p.tol, inits=query_centers)
+                                                  p.max_iter, p.tol, inits=query_centers,
+                                                  inertia=self.inertia)
         return qm, reps, km
 
     def sparse(self, Q, K, V, q_models, reps, key_models, topk: int) -> SparseOut:
@@ -201,7 +212,7 @@ class LayerRunner:
         H = K.shape[0]
         with phase("consolidate"):
             return E.lloyd_batch([K[h] for h in range(H)], [m.centers for m in key_models],
-                                 p.max_iter, p.tol)
+                                 p.max_iter, p.tol, self.inertia)
 
 
 def _stack(heads, keep_bf16=True):
@@ -473,7 +484,7 @@ class LayerSession:
         if H == 0:
             self._plan = "empty"
             return torch.zeros(0, dtype=torch.float64, device=dev), []
-        run = LayerRunner(self.params, None, self.attn_impl)
+        run = LayerRunner(self.params, None, self.attn_impl, inertia=False)
         plan = run.plan(Q, K, self._seeds(H))
         self._plan = plan
         mse = E.mse_batch([K[h] for h in range(H)], plan.key_models)
@@ -507,7 +518,7 @@ class LayerSession:
                 return res
             Q, K, V = (x.to(dev, non_blocking=True) for x in (Q, K, V))
         odt = self.out_dtype or (torch.bfloat16 if Q.dtype == torch.bfloat16 else torch.float32)
-        run = LayerRunner(self.params, odt, self.attn_impl)
+        run = LayerRunner(self.params, odt, self.attn_impl, inertia=False)
         H = Q.shape[0]
         if H == 0:  # a rank without heads of this layer (head sharding)
             if self.t == 0 and self._plan is None:
