@@ -1185,6 +1185,10 @@ k_ufin(const ac_cluster_problem* __restrict__ probs, int d, double tol) {
   // rare: the enclosure straddles an f32 rounding boundary -> the reference's
   // own sequential f64 chain over the members (first member initialises)
   unsigned lanes = __ballot_sync(0xffffffffu, fail != 0);
+  {  // statistic: fallback chains, counted in status[AC_ST_FLAGS] bits 8..
+    const int nf = __reduce_add_sync(0xffffffffu, __popc(fail));
+    if (lane == 0 && nf) atomicAdd(&P.status[AC_ST_FLAGS], nf << 8);
+  }
   while (lanes) {
     const int src = __ffs(lanes) - 1;
     lanes &= lanes - 1;

@@ -80,7 +80,8 @@ for name, src, mode in [("token-order, member-order update", Q, 1),
     stv = st.qb.status.view(H, -1).cpu()
     print(f"== {name}: {a.elapsed_time(b) / args.reps:.3f} ms per chain ({iters} iterations)"
           f"  fix-up rows/launch {int(stv[:, L.ST_FIXUPS].sum()) / 26:.0f}, >2 cand "
-          f"{int(stv[:, L.ST_WIDE].sum()) / 26:.0f} of {H * Ln}")
+          f"{int(stv[:, L.ST_WIDE].sum()) / 26:.0f} of {H * Ln}; split-chain fallback dims "
+          f"{int((stv[:, L.ST_FLAGS] >> 8).sum())} over {iters} iterations")
     for k, (t, c) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:8]:
         print(f"   {t:8.3f} ms  {c:4d}  {k}")
 L.lib().ac_set_update_mode(1)
