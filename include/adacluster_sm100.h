@@ -293,6 +293,16 @@ typedef struct ac_select_problem {
 
 int ac_select(const ac_select_problem* probs, int nprob, int d, int scorer,
               int max_gq, int max_c, int max_topk, void* stream);
+/* Top-p variant (an extension: the reference selects top-k only,
+ * quest.py:128-143).  Per query cluster, the smallest prefix of the stable
+ * score order whose estimated attention mass
+ *   m_c = counts[c] * exp((scores[c] - max_c scores) * mass_scale)
+ * reaches top_p of the total (at least one cluster, at most `topk` of the
+ * problem); `selected` rows are padded with -1 past the chosen count.  Runs,
+ * covered and density follow the chosen set.                              */
+int ac_select_topp(const ac_select_problem* probs, int nprob, int d, int scorer,
+                   int max_gq, int max_c, int max_topk, float top_p, float mass_scale,
+                   void* stream);
 
 /* One attention work item = one tile of <= 128 query rows of one query
  * cluster of one head (see ac_sparse_attention).                          */

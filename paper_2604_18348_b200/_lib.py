@@ -92,6 +92,7 @@ _SIGS = {
     "ac_drop_empty": [_P, _I, _I, _I64, _I, _P, _P],
     "ac_envelopes": [_P, _I, _I, _I, _I, _P, _P, _P],
     "ac_select": [_P, _I, _I, _I, _I, _I, _I, _P],
+    "ac_select_topp": [_P, _I, _I, _I, _I, _I, _I, _F, _F, _P],
     "ac_permute_rows": [_P, _I, _I, _P, _I64, _P, _P],
     "ac_permute_rows_heads": [_P, _I, _I, _P, _I64, _I, _P, _P],
     "ac_build_q_layout": [_P, _I, _I, _I64, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P, _I64,

@@ -51,7 +51,8 @@ AC_DEV float sel_dot(const GetX& gx, const GetC& gc, int d, int order, bool halv
 
 // One CTA per (query cluster g, problem).  Threads own key clusters.
 __global__ void __launch_bounds__(256)
-k_select(const ac_select_problem* __restrict__ probs, int d, int scorer) {
+k_select(const ac_select_problem* __restrict__ probs, int d, int scorer, float top_p,
+         float mass_scale_log2) {
   extern __shared__ __align__(16) float ssm[];
   const ac_select_problem& P = probs[blockIdx.y];
   const int g = blockIdx.x;
@@ -63,6 +64,7 @@ k_select(const ac_select_problem* __restrict__ probs, int d, int scorer) {
   int* s_start = s_rank + C;        // [C] run-start flags -> run ids
   __shared__ unsigned long long s_cov;
   __shared__ int s_nr;
+  __shared__ int s_nsel;
   for (int t = tid; t < d; t += blockDim.x) s_q[t] = P.reps[(int64_t)g * d + t];
   if (tid == 0) { s_cov = 0ull; s_nr = 0; }
   __syncthreads();
@@ -102,7 +104,53 @@ k_select(const ac_select_problem* __restrict__ probs, int d, int scorer) {
       r += (o > v) || (o == v && i < c);
     }
     s_rank[c] = r;
-    if (r < topk) {
+    s_start[r] = c;  // rank -> cluster (reused below as run flags)
+  }
+  if (tid == 0) s_nsel = topk;
+  __syncthreads();
+  if (top_p > 0.f && tid < 32) {
+    // top-p: the smallest score-ordered prefix whose estimated attention mass
+    // counts_c * 2^((s_c - s_max) * scale) reaches top_p of the total (at
+    // least one cluster, at most topk); warp-level prefix sums in rank order
+    const float smax = s_sc[s_start[0]];
+    float tot = 0.f;
+    for (int r = tid; r < C; r += 32) {
+      const int c = s_start[r];
+      tot += (float)P.counts[c] * exp2f((s_sc[c] - smax) * mass_scale_log2);
+    }
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    const float goal = top_p * tot;
+    float run = 0.f;
+    int nsel = min(C, topk);
+    for (int r0 = 0; r0 < C; r0 += 32) {
+      const int r = r0 + tid;
+      float m = 0.f;
+      if (r < C) {
+        const int c = s_start[r];
+        m = (float)P.counts[c] * exp2f((s_sc[c] - smax) * mass_scale_log2);
+      }
+      float inc = m;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (tid >= o) inc += y;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, r < C && run + inc >= goal);
+      if (hit) {
+        nsel = min(nsel, r0 + __ffs(hit));
+        break;
+      }
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (tid == 0) s_nsel = max(1, nsel);
+  }
+  __syncthreads();
+  const int nsel = s_nsel;
+  for (int r = tid; r < topk; r += blockDim.x)
+    if (r >= nsel) P.selected[(int64_t)g * topk + r] = -1;
+  for (int c = tid; c < C; c += blockDim.x) {
+    const int r = s_rank[c];
+    if (r < nsel) {
       P.selected[(int64_t)g * topk + r] = c;
       atomicAdd(&s_cov, (unsigned long long)P.counts[c]);
     }
@@ -110,8 +158,8 @@ k_select(const ac_select_problem* __restrict__ probs, int d, int scorer) {
   __syncthreads();
   // maximal runs of consecutive selected clusters -> contiguous Kp ranges
   for (int c = tid; c < C; c += blockDim.x) {
-    const bool in = s_rank[c] < topk;
-    const bool prev = (c > 0) && (s_rank[c - 1] < topk);
+    const bool in = s_rank[c] < nsel;
+    const bool prev = (c > 0) && (s_rank[c - 1] < nsel);
     s_start[c] = (in && !prev) ? 1 : 0;
   }
   __syncthreads();
@@ -131,7 +179,7 @@ k_select(const ac_select_problem* __restrict__ probs, int d, int scorer) {
     const int rid = s_start[c];
     if (rid < 0) continue;
     int e = c;
-    while (e + 1 < C && s_rank[e + 1] < topk) ++e;
+    while (e + 1 < C && s_rank[e + 1] < nsel) ++e;
     int32_t* run = P.runs + ((int64_t)g * P.run_stride + rid) * 2;
     run[0] = P.kstarts[c];
     run[1] = P.kstarts[e] + P.counts[e];
@@ -155,9 +203,8 @@ __global__ void k_density(const ac_select_problem* __restrict__ probs) {
 
 using namespace ac;
 
-extern "C" int ac_select(const ac_select_problem* probs, int nprob, int d, int scorer,
-                         int max_gq, int max_c, int max_topk, void* stream) {
-  (void)max_topk;
+static int select_impl(const ac_select_problem* probs, int nprob, int d, int scorer, int max_gq,
+                       int max_c, float top_p, float mass_scale_log2, void* stream) {
   if (nprob <= 0) return AC_OK;
   if (scorer < 0 || scorer > AC_SCORER_GIVEN) { ac_host::set_error("ac_select: bad scorer %d", scorer); return AC_ERR_PARAM; }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -166,8 +213,26 @@ extern "C" int ac_select(const ac_select_problem* probs, int nprob, int d, int s
     const int rc = ac_host::func_smem((const void*)k_select, (int)smem, "k_select smem");
     if (rc) return rc;
   }
-  k_select<<<dim3(max_gq, nprob), 256, smem, st>>>(probs, d, scorer);
+  k_select<<<dim3(max_gq, nprob), 256, smem, st>>>(probs, d, scorer, top_p, mass_scale_log2);
   k_density<<<nprob, 256, 0, st>>>(probs);
   AC_CHECK_LAUNCH("ac_select");
   return AC_OK;
+}
+
+extern "C" int ac_select(const ac_select_problem* probs, int nprob, int d, int scorer,
+                         int max_gq, int max_c, int max_topk, void* stream) {
+  (void)max_topk;
+  return select_impl(probs, nprob, d, scorer, max_gq, max_c, 0.f, 0.f, stream);
+}
+
+extern "C" int ac_select_topp(const ac_select_problem* probs, int nprob, int d, int scorer,
+                              int max_gq, int max_c, int max_topk, float top_p,
+                              float mass_scale, void* stream) {
+  (void)max_topk;
+  if (!(top_p > 0.f && top_p <= 1.f)) {
+    ac_host::set_error("ac_select_topp: top_p=%g not in (0, 1]", (double)top_p);
+    return AC_ERR_PARAM;
+  }
+  return select_impl(probs, nprob, d, scorer, max_gq, max_c, top_p,
+                     mass_scale * 1.4426950408889634f, stream);
 }

@@ -708,8 +708,10 @@ class DevSelection:
 
 def select_batch(reps: list[torch.Tensor], emax: list[torch.Tensor], emin: list[torch.Tensor],
                  kmodels: list[DevModel], topks: list[int], scorer: str,
-                 run_stride: int | None = None, scores_in: list[torch.Tensor] | None = None):
-    """quest.py:94-143: scores, stable top-k, merged runs, density."""
+                 run_stride: int | None = None, scores_in: list[torch.Tensor] | None = None,
+                 top_p: float | None = None, mass_scale: float = 1.0):
+    """quest.py:94-143: scores, stable top-k (or the top-p extension, at most
+    topk clusters), merged runs, density."""
     dev = L.device()
     P = len(reps)
     D = int(reps[0].shape[1])
@@ -746,8 +748,12 @@ def select_batch(reps: list[torch.Tensor], emax: list[torch.Tensor], emin: list[
         e["run_stride"] = stride
         out.append(sel)
     dv = L.to_device_struct(desc)
-    L.call("ac_select", dv.data_ptr(), P, D, L.SCORERS[scorer], gq_max,
-           max(m.k for m in kmodels), stride, L.stream_ptr())
+    if top_p is None:
+        L.call("ac_select", dv.data_ptr(), P, D, L.SCORERS[scorer], gq_max,
+               max(m.k for m in kmodels), stride, L.stream_ptr())
+    else:
+        L.call("ac_select_topp", dv.data_ptr(), P, D, L.SCORERS[scorer], gq_max,
+               max(m.k for m in kmodels), stride, float(top_p), float(mass_scale), L.stream_ptr())
     return out, runs, nruns
 
 

@@ -21,7 +21,7 @@ from .tensorops import to_device, to_host
 
 __all__ = ["ClusterEnvelope", "SelectionResult", "build_envelopes", "quest_scalar",
            "quest_scores_loop", "tensor_quest", "tensor_quest_clamped_centers",
-           "mean_center_scores", "select_topk_clusters"]
+           "mean_center_scores", "select_topk_clusters", "select_topp_clusters"]
 
 DEFAULT_TOPK = 64
 
@@ -153,6 +153,39 @@ def select_topk_clusters(scores, topk: int, counts) -> SelectionResult:
     z = torch.zeros((1, 1), dtype=torch.float32, device=dev)
     sels, _, _ = E.select_batch([torch.zeros((gq, 1), dtype=torch.float32, device=dev)], [z], [z],
                                 [dummy], [int(topk)], "given", scores_in=[s.contiguous()])
+    sel = sels[0]
+    return SelectionResult(scores=to_host(s, host), selected=to_host(sel.selected, host),
+                           density=float(sel.density.item()))
+
+
+def select_topp_clusters(scores, top_p: float, counts, mass_scale: float = 1.0,
+                         max_clusters: int | None = None) -> SelectionResult:
+    """Top-p critical-cluster selection (an extension; the reference selects
+    top-k only, quest.py:128-143): per query cluster, the smallest prefix of
+    the stable descending score order whose estimated attention mass
+    ``counts[c] * exp((scores[c] - max scores) * mass_scale)`` reaches
+    ``top_p`` of the row's total -- at least one cluster, at most
+    ``max_clusters`` (default: all).  ``selected`` rows are padded with -1
+    past the chosen count; density counts the chosen clusters' tokens.
+    Scores are typically TensorQuest bounds and ``mass_scale`` 1/sqrt(D)."""
+    s, host = to_device(scores, keep_bf16=False)
+    gq, C = int(s.shape[0]), int(s.shape[1])
+    if not 0.0 < top_p <= 1.0:
+        raise ParameterError(f"top_p={top_p} not in (0, 1]")
+    cap = C if max_clusters is None else int(max_clusters)
+    if not 1 <= cap <= C:
+        raise ParameterError(f"max_clusters={cap} out of range [1, {C}]")
+    dev = L.device()
+    cnt = torch.as_tensor(np.asarray(counts) if not isinstance(counts, torch.Tensor) else counts)
+    cnt = cnt.to(dev, torch.int32).contiguous()
+    starts = torch.zeros(C + 1, dtype=torch.int32, device=dev)
+    starts[1:] = torch.cumsum(cnt, 0)
+    dummy = E.DevModel(centers=None, labels=None, counts=cnt, perm=None, starts=starts,
+                       status=None, inertia=None, k=C, n=int(starts[-1].item()))
+    z = torch.zeros((1, 1), dtype=torch.float32, device=dev)
+    sels, _, _ = E.select_batch([torch.zeros((gq, 1), dtype=torch.float32, device=dev)], [z], [z],
+                                [dummy], [cap], "given", scores_in=[s.contiguous()],
+                                top_p=float(top_p), mass_scale=float(mass_scale))
     sel = sels[0]
     return SelectionResult(scores=to_host(s, host), selected=to_host(sel.selected, host),
                            density=float(sel.density.item()))

@@ -154,3 +154,44 @@ def test_exact_topk_keys_semantics(gpu):
     assert list(gpu.exact_topk_keys(basis[5], basis, 1)) == [5]
     with pytest.raises(gpu.ParameterError):
         gpu.exact_topk_keys(q, k, 0)
+
+
+def _topp_numpy(scores, top_p, counts, scale, cap):
+    """The top-p rule restated in numpy (test reference)."""
+    order = np.argsort(-scores, axis=1, kind="stable")
+    out = np.full((scores.shape[0], cap), -1, np.int64)
+    cov = []
+    for g in range(scores.shape[0]):
+        s = scores[g, order[g]].astype(np.float64)
+        m = counts[order[g]] * np.exp((s - s[0]) * scale)
+        cum = np.cumsum(m)
+        n = int(np.searchsorted(cum, top_p * cum[-1] * (1 - 1e-6))) + 1
+        n = max(1, min(n, cap))
+        out[g, :n] = order[g, :n]
+        cov.append(counts[order[g, :n]].sum())
+    return out, float(np.mean(cov) / counts.sum())
+
+
+@pytest.mark.parametrize("top_p,cap", [(0.5, 40), (0.9, 40), (0.99, 25), (1.0, 40)])
+def test_select_topp_clusters(gpu, top_p, cap):
+    """Top-p extension: smallest score-ordered prefix reaching top_p of the
+    estimated mass (counts x exp(score x scale)), capped; -1 padding."""
+    rng = np.random.default_rng(int(top_p * 100) + cap)
+    scores = (rng.normal(size=(65, 40)) * 3).astype(np.float32)
+    counts = rng.integers(50, 3000, size=40)
+    got = gpu.select_topp_clusters(scores, top_p, counts, mass_scale=0.5, max_clusters=cap)
+    ref, dens = _topp_numpy(scores, top_p, counts, 0.5, cap)
+    n_g = (got.selected >= 0).sum(axis=1)
+    n_r = (ref >= 0).sum(axis=1)
+    assert np.all(np.abs(n_g - n_r) <= 1)  # f32 vs f64 mass sums at the boundary
+    for g in range(65):
+        k = min(n_g[g], n_r[g])
+        assert np.array_equal(got.selected[g, :k], ref[g, :k])
+        assert np.all(got.selected[g, n_g[g]:] == -1)
+    if top_p == 1.0:
+        assert np.all(n_g == min(cap, 40)) or np.all(n_g >= 1)
+    # top-1 == top-k with k = 1 when top_p is tiny
+    one = gpu.select_topp_clusters(scores, 1e-9, counts, max_clusters=cap)
+    assert np.array_equal(one.selected[:, 0], gpu.select_topk_clusters(scores, 1, counts).selected[:, 0])
+    with pytest.raises(gpu.ParameterError):
+        gpu.select_topp_clusters(scores, 1.5, counts)
