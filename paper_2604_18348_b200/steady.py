@@ -176,7 +176,14 @@ class SteadyStep:
         split = int(os.environ.get("AC_STEADY_SPLIT", split))
         self.split = max(1, min(split, H))
         self.hb = (H + self.split - 1) // self.split
-        nblk = (H + self.hb - 1) // self.hb
+        # from pinned host inputs the last head block's data arrives last
+        # (PCIe), so smaller blocks shorten the tail after it: twice the
+        # device-resident split above 200k rows (e2e C3 8.59 vs 8.75 ms, C4
+        # 79.3 vs 80.2; C1 is faster unsplit); AC_STEADY_SPLIT_HOST overrides
+        split_h = self.split * 2 if H * Ln > 200_000 else self.split
+        split_h = max(1, min(int(os.environ.get("AC_STEADY_SPLIT_HOST", split_h)), H))
+        self.hb_host = (H + split_h - 1) // split_h
+        nblk = max((H + self.hb - 1) // self.hb, (H + self.hb_host - 1) // self.hb_host)
         self.streams = [torch.cuda.Stream() for _ in range(2 * nblk)]
         self.fork = torch.cuda.Event()
         self.fork_v = torch.cuda.Event()
@@ -231,7 +238,8 @@ class SteadyStep:
         p = self.p
         kb, qb = self.kb, self.qb
         main = torch.cuda.current_stream()
-        blocks = [(h0, min(H, h0 + self.hb)) for h0 in range(0, H, self.hb)]
+        hb = self.hb_host if host is not None else self.hb
+        blocks = [(h0, min(H, h0 + hb)) for h0 in range(0, H, hb)]
         self.ev[0].record()
         self.fork.record(main)
         # host path: per-block H2D copies on their own stream in the order the
