@@ -191,13 +191,18 @@ WS_FIELDS = {
 
 def workspace_bytes(op: int, *dims: int) -> dict:
     """Per-buffer byte sizes of one problem / launch (ac_workspace_bytes)."""
+    return dict(_workspace_bytes(op, tuple(int(x) for x in dims)))
+
+
+@functools.lru_cache(maxsize=4096)
+def _workspace_bytes(op: int, dims: tuple) -> tuple:
     names = WS_FIELDS.get(op, ())
     d = np.asarray(dims, np.int64)
     f = np.zeros(max(len(names), 1), np.int64)
     tot = int(lib().ac_workspace_bytes(op, d.ctypes.data, len(d), f.ctypes.data, len(names)))
     if tot < 0:
         check(AC_ERR_PARAM, "ac_workspace_bytes")
-    return dict(zip(names, (int(x) for x in f)))
+    return tuple(zip(names, (int(x) for x in f)))
 
 
 def to_device_struct(arr: np.ndarray) -> torch.Tensor:
@@ -205,6 +210,12 @@ def to_device_struct(arr: np.ndarray) -> torch.Tensor:
     raw = np.ascontiguousarray(arr).view(np.uint8)
     host = torch.from_numpy(raw.copy()).pin_memory()
     return host.to(device(), non_blocking=True)
+
+
+def upload(t: torch.Tensor) -> torch.Tensor:
+    """Small host tensor -> device without a stream sync: a pageable copy
+    waits for the stream's queued work; a pinned one is enqueued."""
+    return t.pin_memory().to(device(), non_blocking=True)
 
 
 def dtype_code(t: torch.Tensor) -> int:

@@ -1284,59 +1284,141 @@ __global__ void k_kpp_dist(const ac_cluster_problem* __restrict__ probs, int dty
 // pairwise accumulator r_j = sum_m (x[j+8m] - c[j+8m])^2 in order and
 // pw8_combine folds the 8 (same operations as pw_sum, same bits); each load
 // instruction of a warp touches 4 rows x 8 consecutive elements.
+//
+// Rows whose minimum cannot change are not read: labels[r] holds the centre
+// a whose distance is best[r] (scratch during seeding) and movement[a] =
+// ||c_s - c_a|| rounded down (written by k_kpp_pick).  By the triangle
+// inequality ||x - c_s|| >= ||c_s - c_a|| - ||x - c_a||, so when
+// ||c_s - c_a|| >= 2(1 + 1e-3) sqrt(best) the new distance exceeds best by a
+// factor ~1.004 -- far beyond the ~1e-5 relative rounding of either f32
+// distance -- and np.minimum keeps best, bit for bit.  ~80 % of the rows
+// of a C2/C3 head are skipped this way (keys and queries alike).  A warp
+// tests 32 consecutive rows (coalesced best/labels, the distance table in
+// shared memory), then computes the surviving rows four at a time.
+constexpr int kKppTab = 4096;
 template <int D>
 __global__ void __launch_bounds__(256)
 k_kpp_dist_v(const ac_cluster_problem* __restrict__ probs, int dtype, int s) {
+  __shared__ float s_tab[kKppTab];
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (s + 1 >= P.k || P.status[AC_ST_KPP_STOP] >= 0) return;
-  const int j = threadIdx.x & 7;
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3);
+  const bool prune = s > 0 && P.labels && P.movement;
+  const bool tab_smem = prune && s <= kKppTab;
+  if (tab_smem)
+    for (int t = threadIdx.x; t < s; t += blockDim.x) s_tab[t] = P.movement[t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+  if (r0 >= P.n) return;
+  const int64_t r = r0 + lane;
   const bool ok = r < P.n;
-  const int64_t base = (ok ? r : 0) * D;
+  float b = 0.f;
+  bool need = ok;
+  if (ok && s > 0) {
+    b = P.best[r];
+    if (prune) {
+      const int a = P.labels[r];
+      const float dc = tab_smem ? s_tab[a] : P.movement[a];
+      if ((b == 0.f && !isnan(dc)) || (b >= 1e-30f && dc >= 2.002f * __fsqrt_rn(b))) need = false;
+    }
+  }
+  unsigned mask = __ballot_sync(0xffffffffu, need);
+  const int j = lane & 7, g = lane >> 3;
   const float* c = P.centers + (int64_t)s * D;
-  float xv[D / 8];
-  if (dtype == AC_DTYPE_BF16) {
-    const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(P.x) + base;
+  float cv[D / 8];
 #pragma unroll
-    for (int m = 0; m < D / 8; ++m) xv[m] = __bfloat162float(x[j + 8 * m]);
-  } else {
-    const float* x = reinterpret_cast<const float*>(P.x) + base;
+  for (int m = 0; m < D / 8; ++m) cv[m] = c[j + 8 * m];
+  while (mask) {
+    // rows of this round: the first four surviving rows, one per 8-lane group
+    const unsigned pos = __fns(mask, 0, g + 1);
+    const bool have = pos < 32u;
+    const int sel = have ? (int)pos : 0;
+    for (int q = 0; q < 4 && mask; ++q) mask &= mask - 1;
+    const float bs = __shfl_sync(0xffffffffu, b, sel);
+    const int64_t rs = r0 + sel;
+    float xv[D / 8];
+    if (!have) {
 #pragma unroll
-    for (int m = 0; m < D / 8; ++m) xv[m] = __ldg(x + j + 8 * m);
+      for (int m = 0; m < D / 8; ++m) xv[m] = 0.f;
+    } else if (dtype == AC_DTYPE_BF16) {
+      const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(P.x) + rs * D;
+#pragma unroll
+      for (int m = 0; m < D / 8; ++m) xv[m] = __bfloat162float(x[j + 8 * m]);
+    } else {
+      const float* x = reinterpret_cast<const float*>(P.x) + rs * D;
+#pragma unroll
+      for (int m = 0; m < D / 8; ++m) xv[m] = __ldg(x + j + 8 * m);
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int m = 0; m < D / 8; ++m) {
+      const float df = __fsub_rn(xv[m], cv[m]);
+      acc = m == 0 ? __fmul_rn(df, df) : __fadd_rn(acc, __fmul_rn(df, df));
+    }
+    const float dist = pw8_combine(acc);
+    if (have && j == 0) {
+      if (s == 0) {
+        P.best[rs] = dist;
+        if (P.labels) P.labels[rs] = 0;
+      } else {
+        P.best[rs] = np_minimum(bs, dist);
+        if (prune && dist < bs) P.labels[rs] = s;
+      }
+    }
   }
-  float acc = 0.f;
-#pragma unroll
-  for (int m = 0; m < D / 8; ++m) {
-    const float df = __fsub_rn(xv[m], c[j + 8 * m]);
-    acc = m == 0 ? __fmul_rn(df, df) : __fadd_rn(acc, __fmul_rn(df, df));
-  }
-  const float dist = pw8_combine(acc);
-  if (ok && j == 0) P.best[r] = (s == 0) ? dist : np_minimum(P.best[r], dist);
 }
 
 // total = closest.sum(); p = closest / total; choice(n, p): f64 cumsum,
 // /= cdf[-1], searchsorted(u, 'right').  One CTA of 1024 threads per problem.
-// The f64 prefix sums are computed in parallel; they equal numpy's sequential
-// cumsum exactly whenever every non-zero p >= 2^-29 (all partial sums are then
-// multiples of 2^-52 below 2, hence exact) — otherwise a single thread replays
-// the sequential cumsum.
+//
+// When every non-zero p >= 2^-29 (the normal case), every p is a multiple of
+// 2^-52 below 1 and every partial sum a multiple of 2^-52 below 2: numpy's
+// sequential f64 cumsum is then exact, and equals p * 2^52 summed as int64 in
+// any order.  The search runs in two passes over coalesced 32-element rows:
+//   1. warp w owns a contiguous chunk of rows; each lane sums its column of
+//      the chunk (int64 adds, loads batched 8 rows deep), one warp reduction
+//      per chunk; warp 0 scans the 32 chunk sums and picks the first chunk
+//      whose cdf passes u;
+//   2. that chunk's row sums (all warps), a warp scan over them picks the
+//      row, and one warp scan of the row picks the element.
+// Otherwise (tiny non-zero p) thread 0 replays the sequential f64 cumsum.
+AC_DEV long long warp_incl_scan_i64(long long v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long w = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += w;
+  }
+  return v;
+}
+AC_DEV long long warp_sum_i64(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+AC_DEV long long p_fixed52(float p) {
+  return __double2ll_rn(__dmul_rn((double)p, 4503599627370496.0));  // p * 2^52 (exact)
+}
+constexpr double kTwoM52 = 2.220446049250313e-16;  // 2^-52
+
 __global__ void __launch_bounds__(1024)
 k_kpp_pick(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int s,
-           const double* __restrict__ draws, int max_k) {
+           const double* __restrict__ draws, int max_k, int64_t rows_off) {
   extern __shared__ __align__(16) unsigned char kpsm[];
   const ac_cluster_problem& P = probs[blockIdx.x];
   if (s + 1 >= P.k || P.status[AC_ST_KPP_STOP] >= 0) return;
   const int64_t n = P.n;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nw = (int)(blockDim.x >> 5);
   const float* closest = P.best;
   PwPlan plan{P.plan_n};
   const float total =
-      pw_eval_block<float>(plan, [&](int i) { return closest[i]; }, reinterpret_cast<float*>(kpsm));
+      pw_eval_block_g8<float>(plan, [&](int i) { return closest[i]; }, reinterpret_cast<float*>(kpsm));
   const double draw = draws[(int64_t)blockIdx.x * max_k + s + 1];
   __shared__ long long s_idx;
-  __shared__ int s_inexact;
-  __shared__ double s_pref[1024];
-  __shared__ int s_first;
+  __shared__ int s_inexact, s_chunk;
+  __shared__ long long s_csum[32];  // chunk sums -> inclusive chunk prefixes
+  long long* rsum = reinterpret_cast<long long*>(kpsm + rows_off);  // rows of the chosen chunk
   if (!(total > 0.f)) {
     // `if total <= 0: idx = int(rng.integers(n))` — forced draw or stop
     if (tid == 0) {
@@ -1345,53 +1427,96 @@ k_kpp_pick(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int s
     }
     __syncthreads();
   } else {
-    if (tid == 0) { s_inexact = 0; s_first = INT_MAX; }
-    __syncthreads();
-    const int64_t seg = (n + blockDim.x - 1) / blockDim.x;
-    const int64_t lo = min(n, (int64_t)tid * seg), hi = min(n, lo + seg);
-    double local = 0.0;
-    int inexact = 0;
-    for (int64_t j = lo; j < hi; ++j) {
-      const float p = __fdiv_rn(closest[j], total);
+    const int64_t R = (n + 31) / 32;
+    const int64_t C = (R + nw - 1) / nw;  // rows per chunk
+    auto pval = [&](float c, int& inexact) -> long long {
+      const float p = __fdiv_rn(c, total);
       if (p != 0.f && p < 1.8626451e-09f) inexact = 1;  // 2^-29
-      local = __dadd_rn(local, (double)p);
-    }
-    if (inexact) s_inexact = 1;
-    s_pref[tid] = local;
+      return p_fixed52(p);
+    };
+    if (tid == 0) { s_inexact = 0; s_chunk = -1; }
     __syncthreads();
-    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
-      const double v = (tid >= off) ? s_pref[tid - off] : 0.0;
-      __syncthreads();
-      s_pref[tid] = __dadd_rn(s_pref[tid], v);
-      __syncthreads();
-    }
-    const double last = s_pref[blockDim.x - 1];
-    const double u = draw;
-    if (!s_inexact) {
-      if (hi > lo && __ddiv_rn(s_pref[tid], last) > u) atomicMin(&s_first, tid);
-      __syncthreads();
-      if (tid == s_first) {
-        double run = s_pref[tid] - local;  // exact: all partial sums representable
-        long long idx = hi;
-        for (int64_t j = lo; j < hi; ++j) {
-          run = __dadd_rn(run, (double)__fdiv_rn(closest[j], total));
-          if (__ddiv_rn(run, last) > u) { idx = j; break; }
+    // pass 1: chunk sums
+    int inexact = 0;
+    {
+      const int64_t r0 = (int64_t)warp * C, r1 = min(R, r0 + C);
+      long long acc = 0;
+      for (int64_t rb = r0; rb < r1; rb += 8) {
+        float cl[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int64_t jj = (rb + q) * 32 + lane;
+          cl[q] = (rb + q < r1 && jj < n) ? closest[jj] : 0.f;
         }
-        s_idx = idx;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += pval(cl[q], inexact);
       }
-      if (tid == 0 && s_first == INT_MAX) s_idx = n;  // u beyond the cdf (cannot happen)
+      acc = warp_sum_i64(acc);
+      if (lane == 0) s_csum[warp] = acc;
+    }
+    if (__any_sync(0xffffffffu, inexact) && lane == 0) s_inexact = 1;
+    __syncthreads();
+    if (!s_inexact) {
+      if (warp == 0) {
+        const long long inc = warp_incl_scan_i64(lane < nw ? s_csum[lane] : 0);
+        const double last = (double)__shfl_sync(0xffffffffu, inc, nw - 1) * kTwoM52;  // cdf[-1]
+        const unsigned hit = __ballot_sync(0xffffffffu, lane < nw && __ddiv_rn((double)inc * kTwoM52, last) > draw);
+        if (lane == 0) s_chunk = hit ? __ffs(hit) - 1 : -1;
+        s_csum[lane] = inc;
+      }
+      __syncthreads();
+      const int f = s_chunk;
+      const double last = (double)s_csum[nw - 1] * kTwoM52;
+      if (f >= 0) {
+        // pass 2: row sums of chunk f
+        const int64_t r0 = (int64_t)f * C, r1 = min(R, r0 + C);
+        for (int64_t r = r0 + warp; r < r1; r += nw) {
+          const int64_t jj = r * 32 + lane;
+          long long v = jj < n ? pval(closest[jj], inexact) : 0;
+          v = warp_sum_i64(v);
+          if (lane == 0) rsum[r - r0] = v;
+        }
+        __syncthreads();
+        if (warp == 0) {
+          long long carry = f > 0 ? s_csum[f - 1] : 0;
+          long long idx = -1, base = 0;
+          for (int64_t b = r0; b < r1 && idx < 0; b += 32) {
+            const long long v = (b + lane < r1) ? rsum[b + lane - r0] : 0;
+            const long long inc = warp_incl_scan_i64(v);
+            const unsigned hit = __ballot_sync(
+                0xffffffffu, b + lane < r1 && __ddiv_rn((double)(carry + inc) * kTwoM52, last) > draw);
+            if (hit) {
+              const int l = __ffs(hit) - 1;
+              idx = b + l;  // the row
+              base = carry + __shfl_sync(0xffffffffu, inc - v, l);  // exclusive prefix of the row
+            }
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+          }
+          if (idx >= 0) {
+            const int64_t jj = idx * 32 + lane;
+            const long long v = jj < n ? pval(closest[jj], inexact) : 0;
+            const long long runj = base + warp_incl_scan_i64(v);
+            const unsigned hit =
+                __ballot_sync(0xffffffffu, jj < n && __ddiv_rn((double)runj * kTwoM52, last) > draw);
+            if (lane == 0) s_idx = hit ? idx * 32 + __ffs(hit) - 1 : n;
+          } else if (lane == 0) {
+            s_idx = n;
+          }
+        }
+      } else if (tid == 0) {
+        s_idx = n;  // u beyond the cdf (cannot happen)
+      }
       __syncthreads();
     } else {
-      if (tid == 0) {
-        // sequential replay of numpy's cumsum
+      if (tid == 0) {  // sequential replay of numpy's cumsum
         double run = 0.0;
-        for (int64_t j = 0; j < n; ++j) run = __dadd_rn(run, (double)__fdiv_rn(closest[j], total));
+        for (int64_t j2 = 0; j2 < n; ++j2) run = __dadd_rn(run, (double)__fdiv_rn(closest[j2], total));
         const double lastv = run;
         run = 0.0;
         long long idx = n;
-        for (int64_t j = 0; j < n; ++j) {
-          run = __dadd_rn(run, (double)__fdiv_rn(closest[j], total));
-          if (__ddiv_rn(run, lastv) > u) { idx = j; break; }
+        for (int64_t j2 = 0; j2 < n; ++j2) {
+          run = __dadd_rn(run, (double)__fdiv_rn(closest[j2], total));
+          if (__ddiv_rn(run, lastv) > draw) { idx = j2; break; }
         }
         s_idx = idx;
         P.status[AC_ST_FLAGS] |= 1;  // sequential cumsum fallback used
@@ -1404,6 +1529,20 @@ k_kpp_pick(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int s
   const int64_t ci = min((long long)n - 1, idx);
   for (int t = tid; t < d; t += blockDim.x)
     P.centers[(int64_t)(s + 1) * d + t] = ld_elem(P.x, dtype, ci * d + t);
+  // ||c_{s+1} - c_j|| for j <= s, f64, rounded down to f32: the skip test of
+  // k_kpp_dist_v at step s + 1 (one warp per centre)
+  if (P.movement && P.labels) {
+    for (int jc = warp; jc <= s; jc += nw) {
+      double acc = 0.0;
+      for (int t = lane; t < d; t += 32) {
+        const double df = (double)ld_elem(P.x, dtype, ci * d + t) - (double)P.centers[(int64_t)jc * d + t];
+        acc = fma(df, df, acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) P.movement[jc] = __double2float_rd(sqrt(acc));
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -2058,20 +2197,29 @@ extern "C" int ac_kmeanspp(const ac_cluster_problem* probs, int nprob, int dtype
   cudaStream_t st = S(stream);
   k_status_init<<<(nprob + 127) / 128, 128, 0, st>>>(probs, nprob);
   k_kpp_init<<<nprob, 128, 0, st>>>(probs, dtype, d, draws, max_k);
-  const size_t psm = plan_vals_bytes(max_n, sizeof(float));
-  int rc = set_smem((const void*)k_kpp_pick, psm);
+  // pairwise-tree values, then one int64 per 32-element row of one chunk
+  // (a 32nd of the rows)
+  const int64_t rows_off = (int64_t)((plan_vals_bytes(max_n, sizeof(float)) + 15) & ~size_t(15));
+  const int64_t chunk_rows = ((max_n + 31) / 32 + 31) / 32;
+  const size_t psm = (size_t)(rows_off + chunk_rows * 8);
+  if (psm > 200 * 1024) {
+    ac_host::set_error("ac_kmeanspp: n=%lld too large", (long long)max_n);
+    return AC_ERR_PARAM;
+  }
+  // (static shared memory included: the attribute is needed below 48 KB too)
+  int rc = ac_host::func_smem((const void*)k_kpp_pick, (int)psm, "k_kpp_pick smem");
   if (rc) return rc;
   const bool rows_fast = (d == 64 || d == 128) && (dtype == AC_DTYPE_F32 || dtype == AC_DTYPE_BF16);
   for (int s = 0; s + 1 < max_k; ++s) {
     if (rows_fast) {
-      const dim3 grid((unsigned)((max_n + 31) / 32), nprob);
+      const dim3 grid((unsigned)((max_n + 255) / 256), nprob);
       if (d == 64) k_kpp_dist_v<64><<<grid, 256, 0, st>>>(probs, dtype, s);
       else k_kpp_dist_v<128><<<grid, 256, 0, st>>>(probs, dtype, s);
     } else {
       k_kpp_dist<<<dim3((unsigned)((max_n + 255) / 256), nprob), 256, sizeof(float) * d, st>>>(
           probs, dtype, d, s);
     }
-    k_kpp_pick<<<nprob, 1024, psm, st>>>(probs, dtype, d, s, draws, max_k);
+    k_kpp_pick<<<nprob, 1024, psm, st>>>(probs, dtype, d, s, draws, max_k, rows_off);
   }
   AC_CHECK_LAUNCH("ac_kmeanspp");
   return AC_OK;

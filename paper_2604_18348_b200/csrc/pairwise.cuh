@@ -56,4 +56,59 @@ __device__ T pw_eval_block(const PwPlan plan, const Get& get, T* vals) {
   return r;
 }
 
+
+// Same tree, leaves evaluated by 8-lane groups (four leaves per warp): lane
+// j of a group runs numpy's accumulator r_j = a[j] + a[j+8] + ... in order,
+// the three xor-shuffles fold ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and lane 0
+// adds the n % 8 tail in order -- pw_leaf's operations, so the same bits,
+// with each load instruction touching 4 x 32 contiguous bytes instead of 32
+// scattered words (the one-thread-per-leaf form is bound by L1 wavefronts).
+template <typename T, typename Get>
+__device__ T pw_eval_block_g8(const PwPlan plan, const Get& get, T* vals) {
+  const int L = plan.leaves();
+  const int lane = threadIdx.x & 31, j = lane & 7;
+  for (int base = (threadIdx.x >> 5) * 4; base < L; base += (blockDim.x >> 5) * 4) {
+    const int leaf = base + (lane >> 3);
+    int lo = 0, m = 0;
+    if (leaf < L) {
+      lo = plan.leaf_lo(leaf);
+      m = plan.leaf_lo(leaf + 1) - lo;
+    }
+    const int full = m >= 8 ? m - (m % 8) : 0;
+    T r = T(0);
+    if (full > 0) {
+      // leaves hold <= 128 elements: all 16 loads of a lane are issued first
+      T v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = (8 * q < full) ? get(lo + 8 * q + j) : T(0);
+      r = v[0];
+#pragma unroll
+      for (int q = 1; q < 16; ++q)
+        if (8 * q < full) r = r + v[q];
+    }
+    r = r + __shfl_xor_sync(0xffffffffu, r, 1);
+    r = r + __shfl_xor_sync(0xffffffffu, r, 2);
+    r = r + __shfl_xor_sync(0xffffffffu, r, 4);
+    if (leaf < L && j == 0) {
+      T res = full > 0 ? r : T(0);
+      for (int i = full; i < m; ++i) res = res + get(lo + i);
+      vals[leaf] = res;
+    }
+  }
+  __syncthreads();
+  const int H = plan.levels();
+  const int32_t* nd = plan.nodes();
+  for (int h = 0; h < H; ++h) {
+    const int b = plan.level_begin(h), e = plan.level_begin(h + 1);
+    for (int jn = b + threadIdx.x; jn < e; jn += blockDim.x) {
+      const int dst = nd[3 * jn], a = nd[3 * jn + 1], c = nd[3 * jn + 2];
+      vals[dst] = vals[a] + vals[c];
+    }
+    __syncthreads();
+  }
+  T res = vals[plan.root()];
+  __syncthreads();
+  return res;
+}
+
 }  // namespace ac

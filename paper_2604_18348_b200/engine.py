@@ -39,8 +39,12 @@ def _draws(seed: int, n: int, k: int, forced_from: int | None = None) -> np.ndar
     rng = np.random.default_rng(seed)
     out = np.empty(max(k, 1), np.float64)
     out[0] = float(rng.integers(n))
+    if forced_from is None:
+        if k > 1:
+            out[1:k] = rng.random(k - 1)  # the same stream as k - 1 scalar draws
+        return out
     for s in range(1, k):
-        if forced_from is not None and s >= forced_from:
+        if s >= forced_from:
             out[s] = -(float(rng.integers(n)) + 1.0)
         else:
             out[s] = rng.random()
@@ -265,11 +269,15 @@ def _group_by_order(ns, ks, D):
 # k-means / Lloyd
 # ---------------------------------------------------------------------------
 def kmeans_batch(xs: list[torch.Tensor], ks: list[int], seeds: list[int], max_iter: int,
-                 tol: float, inertia: bool = True) -> list[DevModel]:
+                 tol: float, inertia: bool = True, stops_out: list | None = None) -> list[DevModel]:
     """clustering.py:155-167 for every problem (k-means++ then Lloyd).
     ``inertia=False``: no inertia_history (callers that never read it -- the
     streaming sessions and the multi-stage rounds -- get the labels-only
-    assignment, same labels / centres / n_iter)."""
+    assignment, same labels / centres / n_iter).  ``stops_out``: instead of
+    reading the k-means++ `total <= 0` stop flags on the host (a sync), append
+    them (device int32 tensors) to this list; a caller that finds any flag
+    >= 0 must redo the call without ``stops_out`` (sync-free enqueue, used to
+    run the query clustering concurrently with the keys')."""
     out: list[DevModel | None] = [None] * len(xs)
     D = int(xs[0].shape[1])
     for idx in _group_by_order([x.shape[0] for x in xs], ks, D):
@@ -281,11 +289,15 @@ def kmeans_batch(xs: list[torch.Tensor], ks: list[int], seeds: list[int], max_it
         draws = np.zeros((len(idx), mk), np.float64)
         for j, (x, k, s) in enumerate(zip(sub_x, sub_k, sub_s)):
             draws[j, :k] = _draws(s, int(x.shape[0]), k)
-        dd = torch.from_numpy(draws).to(L.device(), non_blocking=True)
+        dd = L.upload(torch.from_numpy(draws))
         b.kmeanspp(dd, mk)
-        # k-means++ `total <= 0` replay (all remaining points coincide with a
-        # chosen centre): rare; requires a host look at the stop flags
-        stops = b.status.view(b.P, L.STATUS_WORDS)[:, L.ST_KPP_STOP].cpu().numpy()
+        if stops_out is not None:
+            stops_out.append(b.status.view(b.P, L.STATUS_WORDS)[:, L.ST_KPP_STOP].clone())
+            stops = np.full(1, -1)
+        else:
+            # k-means++ `total <= 0` replay (all remaining points coincide with
+            # a chosen centre): rare; requires a host look at the stop flags
+            stops = b.status.view(b.P, L.STATUS_WORDS)[:, L.ST_KPP_STOP].cpu().numpy()
         if (stops >= 0).any():
             for j in np.flatnonzero(stops >= 0):
                 draws[j, :sub_k[j]] = _draws(sub_s[j], int(sub_x[j].shape[0]), sub_k[j],
@@ -344,7 +356,7 @@ def segment_means(xs: list[torch.Tensor], models: list[DevModel]) -> list[torch.
         e["n"] = m.n
         e["k"] = m.k
     dv = L.to_device_struct(desc)
-    ptrs = torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64).to(L.device())
+    ptrs = L.upload(torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64))
     L.call("ac_segment_mean", dv.data_ptr(), len(xs), L.dtype_code(xs[0]), int(xs[0].shape[1]),
            max(m.k for m in models), ptrs.data_ptr(), L.stream_ptr())
     return outs
@@ -352,11 +364,11 @@ def segment_means(xs: list[torch.Tensor], models: list[DevModel]) -> list[torch.
 
 def cluster_queries_batch(qs: list[torch.Tensor], num_clusters: list[int], seeds: list[int],
                           max_iter: int, tol: float, inits: list[torch.Tensor] | None = None,
-                          inertia: bool = True):
+                          inertia: bool = True, stops_out: list | None = None):
     """clustering.py:182-200: normalise, cluster (cold or warm), representatives."""
     qns = [l2norm(q)[0] for q in qs]
     if inits is None:
-        models = kmeans_batch(qns, num_clusters, seeds, max_iter, tol, inertia)
+        models = kmeans_batch(qns, num_clusters, seeds, max_iter, tol, inertia, stops_out)
     else:
         models = lloyd_batch(qns, inits, max_iter, tol, inertia)
     reps = segment_means(qns, models)
@@ -621,9 +633,9 @@ def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0:
             e["k"] = m.k
             outs.append(torch.empty(s["size"], dtype=torch.int64, device=dev))
         dv = L.to_device_struct(desc)
-        tau32 = torch.tensor([np.float32(taus[h]) for h in todo], dtype=F32).to(dev)
-        pin = torch.tensor([st[h]["pool"].data_ptr() for h in todo], dtype=torch.int64).to(dev)
-        pout = torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64).to(dev)
+        tau32 = L.upload(torch.tensor([np.float32(taus[h]) for h in todo], dtype=F32))
+        pin = L.upload(torch.tensor([st[h]["pool"].data_ptr() for h in todo], dtype=torch.int64))
+        pout = L.upload(torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64))
         cnt = torch.empty(len(todo), dtype=torch.int64, device=dev)
         L.call("ac_retire", dv.data_ptr(), len(todo), dt, D, max(st[h]["size"] for h in todo),
                tau32.data_ptr(), pin.data_ptr(), pout.data_ptr(), cnt.data_ptr(), L.stream_ptr())
@@ -690,8 +702,8 @@ def envelopes_batch(ks: list[torch.Tensor], models: list[DevModel]):
         e["n"] = m.n
         e["k"] = m.k
     dv = L.to_device_struct(desc)
-    pmax = torch.tensor([t.data_ptr() for t in emax], dtype=torch.int64).to(L.device())
-    pmin = torch.tensor([t.data_ptr() for t in emin], dtype=torch.int64).to(L.device())
+    pmax = L.upload(torch.tensor([t.data_ptr() for t in emax], dtype=torch.int64))
+    pmin = L.upload(torch.tensor([t.data_ptr() for t in emin], dtype=torch.int64))
     L.call("ac_envelopes", dv.data_ptr(), len(ks), L.dtype_code(ks[0]), D,
            max(m.k for m in models), pmax.data_ptr(), pmin.data_ptr(), L.stream_ptr())
     return emax, emin
@@ -791,7 +803,7 @@ def sparse_attention_heads(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
            L.stream_ptr())
     L.call("ac_permute_rows_heads", va.data_ptr(), dt, da, kperm.data_ptr(), Ln, H, vp.data_ptr(),
            L.stream_ptr())
-    gq = torch.tensor([m.k for m in qmodels], dtype=I32).to(dev)
+    gq = L.upload(torch.tensor([m.k for m in qmodels], dtype=I32))
     gq_max = int(runs.shape[1])
     topk_max = int(runs.shape[2])
     qperm = torch.stack([m.perm for m in qmodels])

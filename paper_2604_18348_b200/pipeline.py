@@ -153,6 +153,10 @@ class LayerRunner:
         # which the labels-only path recomputes in one CTA per problem
         # (measured: C2 step 0 99 -> 145 ms when cold passes skipped it)
         self.inertia = inertia
+        # the cold query k-means (65 centres, k-means++ seeds) with the
+        # labels-only assignment when inertia is not exported; AC_COLD_Q_INERTIA=1 A/B
+        import os
+        self.cold_q_inertia = inertia or os.environ.get("AC_COLD_Q_INERTIA") == "1"
 
     def plan(self, Q: torch.Tensor, K: torch.Tensor, seeds: list[int]) -> LayerPlan:
         """_plan_head (pipeline.py:168-185) for every head."""
@@ -160,18 +164,45 @@ class LayerRunner:
         H, Ln, _ = Q.shape
         qs = [Q[h] for h in range(H)]
         ks = [K[h] for h in range(H)]
-        with phase("plan_queries"):
+        # the query clustering (no host decisions) is enqueued sync-free on a
+        # side stream and overlaps the key side, whose multi-stage rounds
+        # read results on the host (C2 step 0: 22 + 26 ms -> concurrent)
+        # The key side (the critical path: its multi-stage rounds read
+        # results on the host) runs on a high-priority stream so that the
+        # concurrent query chain only fills the SMs it leaves idle.
+        main = torch.cuda.current_stream()
+        side, hi = _side_stream(), _side_stream(high=True)
+        side.wait_stream(main)
+        hi.wait_stream(main)
+        stops: list = []
+        kstops: list = []
+        kc = min(p.uniform_key_clusters if p.uniform_key_clusters is not None else p.m0, Ln)
+        # keys first (sync-free k-means: stop flags read later), then the
+        # query chain is enqueued while the key kernels already run
+        with phase("plan_stage0"), torch.cuda.stream(hi):
+            s0 = E.kmeans_batch(ks, [kc] * H, seeds, p.max_iter, p.tol, stops_out=kstops)
+        with phase("plan_queries"), torch.cuda.stream(side):
+            qm, reps, _ = E.cluster_queries_batch(qs, [min(p.q_clusters, Ln)] * H, seeds,
+                                                  p.max_iter, p.tol, inertia=self.cold_q_inertia,
+                                                  stops_out=stops)
+        with torch.cuda.stream(hi):
+            if any(bool((t >= 0).any()) for t in kstops):  # rare k-means++ stop: host replay
+                s0 = E.kmeans_batch(ks, [kc] * H, seeds, p.max_iter, p.tol)
+            if p.uniform_key_clusters is not None:
+                km = s0
+                taus = [None] * H
+            else:
+                with phase("plan_tau"):
+                    taus = [float(t) for t in E.tau_batch(ks, s0, p.tau_factor).cpu().numpy()]
+                with phase("plan_multistage"):
+                    km = E.multi_stage_batch(ks, taus, p.n_max, kc, seeds, p.max_iter, p.tol, s0)
+        main.wait_stream(side)
+        main.wait_stream(hi)
+        _adopt(main, qm, reps)
+        _adopt(main, km, [])
+        if any(bool((t >= 0).any()) for t in stops):  # rare k-means++ stop: redo with host replay
             qm, reps, _ = E.cluster_queries_batch(qs, [min(p.q_clusters, Ln)] * H, seeds,
                                                   p.max_iter, p.tol)
-        if p.uniform_key_clusters is not None:
-            km = E.kmeans_batch(ks, [min(p.uniform_key_clusters, Ln)] * H, seeds, p.max_iter, p.tol)
-            return LayerPlan(qm, reps, km, [None] * H)
-        m0 = min(p.m0, Ln)
-        with phase("plan_stage0"):
-            s0 = E.kmeans_batch(ks, [m0] * H, seeds, p.max_iter, p.tol)
-            taus = [float(t) for t in E.tau_batch(ks, s0, p.tau_factor).cpu().numpy()]
-        with phase("plan_multistage"):
-            km = E.multi_stage_batch(ks, taus, p.n_max, m0, seeds, p.max_iter, p.tol, s0)
         return LayerPlan(qm, reps, km, taus)
 
     def warm(self, Q: torch.Tensor, K: torch.Tensor, key_centers: list, query_centers: list):
@@ -213,6 +244,26 @@ class LayerRunner:
         with phase("consolidate"):
             return E.lloyd_batch([K[h] for h in range(H)], [m.centers for m in key_models],
                                  p.max_iter, p.tol, self.inertia)
+
+
+_SIDE: dict = {}
+
+
+def _side_stream(high: bool = False) -> torch.cuda.Stream:
+    key = (torch.cuda.current_device(), high)
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=key[0], priority=-1 if high else 0)
+    return _SIDE[key]
+
+
+def _adopt(stream, models, reps) -> None:
+    """Tensors made on the side stream and used on ``stream`` from now on:
+    keep the caching allocator from reusing them before ``stream`` is done."""
+    for m in models:
+        for t in (m.centers, m.labels, m.counts, m.perm, m.starts, m.status, m.inertia):
+            t.record_stream(stream)
+    for r in reps:
+        r.record_stream(stream)
 
 
 def _stack(heads, keep_bf16=True):

@@ -8,6 +8,7 @@ milliseconds per phase.  No-op (and sync-free) when no timer is active.
 from __future__ import annotations
 
 import contextlib
+import time
 from collections import defaultdict
 
 import torch
@@ -18,6 +19,7 @@ _ACTIVE: "PhaseTimer | None" = None
 class PhaseTimer:
     def __init__(self):
         self.events = defaultdict(list)
+        self.host = defaultdict(float)  # host seconds inside each phase
 
     def __enter__(self):
         global _ACTIVE
@@ -37,6 +39,9 @@ class PhaseTimer:
             out[name] = sum(a.elapsed_time(b) for a, b in pairs)
         return out
 
+    def host_ms(self) -> dict:
+        return {k: v * 1e3 for k, v in self.host.items()}
+
     def counts(self) -> dict:
         return {k: len(v) for k, v in self.events.items()}
 
@@ -50,8 +55,10 @@ def phase(name: str):
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
+    h0 = time.perf_counter()
     try:
         yield
     finally:
         b.record()
+        t.host[name] += time.perf_counter() - h0
         t.events[name].append((a, b))
