@@ -527,8 +527,9 @@ def run_layer(args, cfg, world, rank, local):
     first.step_local(*dev_in[0])
     barrier()
     cold_first_ms = (time.perf_counter() - tf) * 1e3
+    # (the first session's buffers go back to the caching allocator: the
+    # timed cold step is a new layer's step 0 in a running process)
     del first
-    torch.cuda.empty_cache()
     shard = ShardedLayerSession(H, params, seed=0, layer=0, out_dtype=tdt)
     sess = shard.session
 

@@ -658,7 +658,7 @@ k_post(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int iter,
     PwPlan plan{P.plan_n};
     float* vals = reinterpret_cast<float*>(psm);
     const float* best = P.best;
-    const float s = pw_eval_block<float>(plan, [&](int i) { return best[i]; }, vals);
+    const float s = pw_eval_block_g8<float>(plan, [&](int i) { return best[i]; }, vals);
     if (tid == 0) P.inertia[iter] = s;
   }
 
@@ -1554,7 +1554,7 @@ k_reduce_best(const ac_cluster_problem* __restrict__ probs, float* sum_out, floa
   const ac_cluster_problem& P = probs[blockIdx.x];
   const float* best = P.best;
   PwPlan plan{P.plan_n};
-  const float s = pw_eval_block<float>(plan, [&](int i) { return best[i]; },
+  const float s = pw_eval_block_g8<float>(plan, [&](int i) { return best[i]; },
                                        reinterpret_cast<float*>(rsm));
   if (threadIdx.x == 0) {
     if (sum_out) sum_out[blockIdx.x] = s;
@@ -1584,7 +1584,7 @@ k_reduce_dscratch(const ac_cluster_problem* __restrict__ probs, double factor, d
   const ac_cluster_problem& P = probs[blockIdx.x];
   const double* v = P.dscratch;
   PwPlan plan{P.plan_n};
-  const double s = pw_eval_block<double>(plan, [&](int i) { return v[i]; },
+  const double s = pw_eval_block_g8<double>(plan, [&](int i) { return v[i]; },
                                          reinterpret_cast<double*>(dsm));
   if (threadIdx.x == 0) out[blockIdx.x] = __dmul_rn(factor, __ddiv_rn(s, (double)P.n));
 }
