@@ -47,6 +47,13 @@ constexpr int NBAR = 1 + 2 * STAGES + 2 + 2 + 2;
 constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
 constexpr int SMEM = OFF_MISC + 16 + 1024;
 constexpr uint32_t COL_S = 0, COL_O = 256;
+#ifndef AC_F128_INORDER
+// 1: S_t(j+1) is issued right behind PV_t(j) without waiting for its
+// completion -- tcgen05.mma ops of one thread execute in issue order, so the
+// S write lands after PV's read of the aliased P columns; the softmax's
+// s_full commit still covers PV_t(j) (a commit tracks all prior MMAs)
+#define AC_F128_INORDER 1
+#endif
 
 AC_DEV void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                     uint32_t accum) {
@@ -221,8 +228,10 @@ k_attn_fa4_d128(const __grid_constant__ CUtensorMap tmq, const __grid_constant__
           if (j > 0) {
             issue_pv(1, j - 1, (j - 1) % STAGES);
             umma_commit(kv_empty + (j - 1) % STAGES);  // last reader of stage j-1
+#if !AC_F128_INORDER
             mbar_wait_sleep(o_done + 1, (j - 1) & 1, 74);
             fence_after();
+#endif
           }
           issue_s(1, st);
         } else if (j > 0) {
@@ -232,7 +241,9 @@ k_attn_fa4_d128(const __grid_constant__ CUtensorMap tmq, const __grid_constant__
         if (j + 1 < n) {
           const int st1 = (j + 1) % STAGES;
           mbar_wait_sleep(kv_full + st1, ((j + 1) / STAGES) & 1, 75);
+#if !AC_F128_INORDER
           mbar_wait_sleep(o_done + 0, j & 1, 76);
+#endif
           fence_after();
           issue_s(0, st1);
         }
