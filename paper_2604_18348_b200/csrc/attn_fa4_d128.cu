@@ -22,11 +22,12 @@
 // clk/tile on the MUFU) and the MMAs (~1080 clk/tile) are balanced.
 #include <cfloat>
 
-#include "tc_common.cuh"
+#include "attn_common.cuh"
 
 namespace ac {
 namespace f128 {
 using namespace ac::tc;
+using namespace ac::attn;
 
 constexpr int D = 128;
 constexpr int KB = D / 64;  // SW128 atoms per row
@@ -47,6 +48,9 @@ constexpr int NBAR = 1 + 2 * STAGES + 2 + 2 + 2;
 constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
 constexpr int SMEM = OFF_MISC + 16 + 1024;
 constexpr uint32_t COL_S = 0, COL_O = 256;
+#ifndef AC_F128_POLY
+#define AC_F128_POLY 1  // of every 8 exp2 pairs, this many on the FMA pipe (polynomial)
+#endif
 #ifndef AC_F128_INORDER
 // 1: S_t(j+1) is issued right behind PV_t(j) without waiting for its
 // completion -- tcgen05.mma ops of one thread execute in issue order, so the
@@ -54,63 +58,6 @@ constexpr uint32_t COL_S = 0, COL_O = 256;
 // s_full commit still covers PV_t(j) (a commit tracks all prior MMAs)
 #define AC_F128_INORDER 1
 #endif
-
-AC_DEV void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                    uint32_t accum) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-AC_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16};\n" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
-      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
-      "r"(r[15])
-      : "memory");
-}
-AC_DEV uint64_t pk2(float a, float b) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-AC_DEV void up2(uint64_t v, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-AC_DEV uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-AC_DEV uint64_t add2(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-AC_DEV uint32_t pack_bf16(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-
-struct TileIter {
-  const int32_t* runs;
-  int nruns, r, s, e;
-  AC_DEV TileIter(const int32_t* runs_, int nruns_) : runs(runs_), nruns(nruns_), r(-1), s(0), e(0) {}
-  AC_DEV bool next(int& start, int& nk) {
-    while (s >= e) {
-      if (++r >= nruns) return false;
-      s = runs[2 * r];
-      e = runs[2 * r + 1];
-    }
-    start = s;
-    nk = min(BN, e - s);
-    s += BN;
-    return true;
-  }
-};
 
 __global__ void __launch_bounds__(THREADS, 1)
 k_attn_fa4_d128(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
@@ -318,9 +265,14 @@ k_attn_fa4_d128(const __grid_constant__ CUtensorMap tmq, const __grid_constant__
           for (int i = 0; i < 16; ++i) {
             const uint64_t x =
                 fma2(pk2(__uint_as_float(sr[ch][2 * i]), __uint_as_float(sr[ch][2 * i + 1])), sc, nm);
-            float x0, x1;
+            float x0, x1, p0, p1;
             up2(x, x0, x1);
-            const float p0 = ex2(x0), p1 = ex2(x1);
+            if ((i & 7) < AC_F128_POLY) {
+              exp2_poly2(x0, x1, p0, p1);
+            } else {
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
             if (i & 1) acc1 = add2(acc1, pk2(p0, p1));
             else acc0 = add2(acc0, pk2(p0, p1));
             sr[ch][i] = pack_bf16(p0, p1);
