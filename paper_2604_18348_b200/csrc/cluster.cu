@@ -870,9 +870,18 @@ k_update(const ac_cluster_problem* __restrict__ probs, int dtype, int d, double 
 // stage), so ~3 x 32 rows per centre are in flight while the current stage
 // is added; hundreds of centres run concurrently and the kernel is bound by
 // the gather bandwidth, not by the f64 add latency.
-constexpr int kUpdWRows = 32;
-constexpr int kUpdWStages = 3;
-constexpr int kUpdWarps = 4;  // centres per CTA
+#ifndef AC_UPD_ROWS
+#define AC_UPD_ROWS 32
+#endif
+#ifndef AC_UPD_STAGES
+#define AC_UPD_STAGES 3
+#endif
+constexpr int kUpdWRows = AC_UPD_ROWS;
+constexpr int kUpdWStages = AC_UPD_STAGES;
+#ifndef AC_UPD_WARPS
+#define AC_UPD_WARPS 4
+#endif
+constexpr int kUpdWarps = AC_UPD_WARPS;  // centres per CTA
 
 inline size_t update_w_smem(int d, int dtype) {
   const int esz = dtype == AC_DTYPE_BF16 ? 2 : 4;
