@@ -871,7 +871,7 @@ k_update(const ac_cluster_problem* __restrict__ probs, int dtype, int d, double 
 // is added; hundreds of centres run concurrently and the kernel is bound by
 // the gather bandwidth, not by the f64 add latency.
 #ifndef AC_UPD_ROWS
-#define AC_UPD_ROWS 32
+#define AC_UPD_ROWS 16  // rows per ring stage (C4: 76.3 vs 77.9 ms with 32; C2/C3 neutral)
 #endif
 #ifndef AC_UPD_STAGES
 #define AC_UPD_STAGES 3
