@@ -60,13 +60,23 @@ constexpr int OFF_V = OFF_K + STAGES * KV_BYTES;
 constexpr int OFF_BAR = OFF_V + STAGES * KV_BYTES;
 constexpr int NBAR = 1 + 2 * STAGES + 2 + 2 + 2 + 2;
 constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
-constexpr int SMEM = OFF_MISC + 16 + 1024;
+constexpr int OFF_RUNS = OFF_MISC + 16;  // the item's key runs (<= kRunsSmem), read by every role
+constexpr int kRunsSmem = 128;
+constexpr int SMEM = OFF_RUNS + 8 * kRunsSmem + 1024;
 constexpr uint32_t COL_S = 0, COL_O = 256, COL_P = 384;
 #ifndef AC_FA4_ORDER
 #define AC_FA4_ORDER 1  // MMA issue order per K tile (0: S0 S1 PV0 PV1, 1: S0 PV0 S1 PV1)
 #endif
 #ifndef AC_FA4_LATE_WAIT
 #define AC_FA4_LATE_WAIT 1  // wait for PV_t(j-1) after the exponentials (P kept in registers)
+#endif
+#ifndef AC_FA4_SPIN
+#define AC_FA4_SPIN 0  // softmax warps spin on their barriers instead of sleeping
+#endif
+#if AC_FA4_SPIN
+#define SM_WAIT(b, p, tag) mbar_wait(b, p, tag)
+#else
+#define SM_WAIT(b, p, tag) mbar_wait_sleep(b, p, tag)
 #endif
 #ifndef AC_FA4_POLY
 #define AC_FA4_POLY 1  // of every 8 exp2 pairs, this many on the FMA pipe (polynomial)
@@ -111,12 +121,18 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  int32_t* s_runs = reinterpret_cast<int32_t*>(sm + OFF_RUNS);
+  const bool runs_smem = it.nruns <= kRunsSmem;
+  if (runs_smem)
+    for (int i = threadIdx.x; i < 2 * it.nruns; i += blockDim.x) s_runs[i] = runs[2 * it.run0 + i];
   if (warp == W_MMA) tmem_alloc(tmem_slot, 512);
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int32_t* iruns = runs + 2 * it.run0;
+  // (the tile walk reads the runs at every run change: from shared memory,
+  // not a dependent global load on the softmax warps' critical path)
+  const int32_t* iruns = runs_smem ? s_runs : runs + 2 * it.run0;
   const int64_t krow0 = (int64_t)it.head * L;
 
   if (warp == W_TMA) {
@@ -262,7 +278,7 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
       TileIter ti(iruns, it.nruns);
       int start, nk;
       while (ti.next(start, nk)) {
-        mbar_wait_sleep(s_full + t, j & 1, 44);
+        SM_WAIT(s_full + t, j & 1, 44);
         fence_after();
         uint32_t sr[BN / 32][32];
 #pragma unroll
@@ -290,7 +306,7 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
 #if !AC_FA4_LATE_WAIT
         // P_t / O_t are free once the previous tile's PV has completed
         if (j > 0) {
-          mbar_wait_sleep(o_done + t, (j - 1) & 1, 45);
+          SM_WAIT(o_done + t, (j - 1) & 1, 45);
           fence_after();
         }
 #endif
@@ -348,7 +364,7 @@ k_attn_fa4(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUte
         // P_t / O_t are free once the previous tile's PV has completed: the
         // exponentials above ran while PV_t(j-1) was still on the tensor core
         if (j > 0) {
-          mbar_wait_sleep(o_done + t, (j - 1) & 1, 45);
+          SM_WAIT(o_done + t, (j - 1) & 1, 45);
           fence_after();
         }
 #pragma unroll
