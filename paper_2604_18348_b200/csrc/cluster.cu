@@ -2156,8 +2156,20 @@ static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int
   int rc = prepare_impl(probs, nprob, dtype, d, max_n, max_k, (lflags & AC_LLOYD_PREPARED) != 0,
                         stream);
   if (rc) return rc;
+  // host copy of the active flags for polling (kept across calls: a
+  // cudaMallocHost per call costs more than the iterations it saves)
+  thread_local int32_t* t_pinned = nullptr;
+  thread_local int t_pinned_n = 0;
   int32_t* pinned = nullptr;
-  if (poll_every > 0 && host_probs) cudaMallocHost(&pinned, sizeof(int32_t) * nprob);
+  if (poll_every > 0 && host_probs) {
+    if (t_pinned_n < nprob) {
+      if (t_pinned) cudaFreeHost(t_pinned);
+      t_pinned = nullptr;
+      t_pinned_n = 0;
+      if (cudaMallocHost(&t_pinned, sizeof(int32_t) * nprob) == cudaSuccess) t_pinned_n = nprob;
+    }
+    pinned = t_pinned;
+  }
   for (int it = 0; it < max_iter; ++it) {
     // ||c||^2 is current: prepare wrote it, then every centroid update does
     if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0, kAssignCcValid | lo_flag, order,
@@ -2178,7 +2190,6 @@ static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int
       if (!any) break;
     }
   }
-  if (pinned) cudaFreeHost(pinned);
   if (rc) return rc;
   if ((rc = assign_impl(probs, nprob, dtype, d, max_n, max_k, 0,
                         AC_ASSIGN_ALL | kAssignCcValid | lo_flag, order, host_probs, st)))

@@ -17,6 +17,7 @@ pipeline.py:154-275.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -94,8 +95,10 @@ class Batch:
         self.kcaps = [int(c) for c in (kcaps or ks)]
         self.max_iter = max(int(max_iter), 1)
         self.orders = [L.gemm_order(n, k, self.D) for n, k in zip(self.ns, self.ks)]
-        if len(set(self.orders)) != 1:
-            raise ParameterError("batch mixes GEMM accumulation orders")
+        # the general (OpenBLAS sgemm) order has its own kernels; the small-
+        # shape orders share k_assign_generic, which reads each problem's order
+        if len({o == L.ORDER_SEQ for o in self.orders}) != 1:
+            raise ParameterError("batch mixes the general GEMM order with small-shape orders")
         N, K, D, P = sum(self.ns), sum(self.kcaps), self.D, self.P
         tiles = [(n + TILE - 1) // TILE for n in self.ns]
         # buffer sizes from the C-ABI's workspace query (ac_workspace_bytes),
@@ -259,9 +262,11 @@ def batch_buffer_bytes(ns, kcaps, d: int, dtype: int, max_iter: int) -> dict:
 
 
 def _group_by_order(ns, ks, D):
-    groups: dict[int, list[int]] = {}
+    """Problems that can share one batch: the general GEMM order apart from
+    the small-shape orders (LANES16 / GEMV8 problems batch together)."""
+    groups: dict[bool, list[int]] = {}
     for i, (n, k) in enumerate(zip(ns, ks)):
-        groups.setdefault(L.gemm_order(n, k, D), []).append(i)
+        groups.setdefault(L.gemm_order(n, k, D) == L.ORDER_SEQ, []).append(i)
     return list(groups.values())
 
 
@@ -269,7 +274,8 @@ def _group_by_order(ns, ks, D):
 # k-means / Lloyd
 # ---------------------------------------------------------------------------
 def kmeans_batch(xs: list[torch.Tensor], ks: list[int], seeds: list[int], max_iter: int,
-                 tol: float, inertia: bool = True, stops_out: list | None = None) -> list[DevModel]:
+                 tol: float, inertia: bool = True, stops_out: list | None = None,
+                 poll_every: int = 0) -> list[DevModel]:
     """clustering.py:155-167 for every problem (k-means++ then Lloyd).
     ``inertia=False``: no inertia_history (callers that never read it -- the
     streaming sessions and the multi-stage rounds -- get the labels-only
@@ -305,7 +311,7 @@ def kmeans_batch(xs: list[torch.Tensor], ks: list[int], seeds: list[int], max_it
             dd = torch.from_numpy(draws).to(L.device())
             b.kmeanspp(dd, mk)
         if inertia:
-            b.lloyd(max_iter, tol)
+            b.lloyd(max_iter, tol, poll_every)
         else:
             b.lloyd_range(0, b.P, max_iter, tol, inertia=False)
         for j, i in enumerate(idx):
@@ -544,6 +550,9 @@ class _RunningAssignBatch:
         return out
 
 
+_MS_POLL = int(os.environ.get("AC_MS_POLL", "4"))  # C3 cold 108 -> 98 ms (8: 102)
+
+
 def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0: int,
                       seeds: list[int], max_iter: int, tol: float,
                       stage0: list[DevModel | None], schedule=None) -> list[DevModel]:
@@ -609,8 +618,12 @@ def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0:
                 subx[h] = sub
                 need.append(h)
         if need:
+            # small late-round problems converge in a few iterations: poll
+            # the active flags every _MS_POLL iterations instead of launching
+            # all max_iter iterations
             ms = kmeans_batch([subx[h] for h in need], [st[h]["m_t"] for h in need],
-                              [seeds[h] + st[h]["rnd"] for h in need], max_iter, tol)
+                              [seeds[h] + st[h]["rnd"] for h in need], max_iter, tol,
+                              poll_every=_MS_POLL)
             for h, m in zip(need, ms):
                 st[h]["model"], st[h]["sub"] = m, subx[h]
         # retire: U = U[dist >= tau] (f32 compare, NEP 50)
