@@ -654,16 +654,21 @@ def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0:
                tau32.data_ptr(), pin.data_ptr(), pout.data_ptr(), cnt.data_ptr(), L.stream_ptr())
         run.add(todo, [st[h]["model"].centers for h in todo])
         mses = run.mean_best(todo)
+        zero = torch.zeros((), dtype=I32, device=dev)
+        nits = torch.stack([zero if st[h]["model"].host_iters is not None
+                            else st[h]["model"].status[L.ST_NITER] for h in todo])
         for h in todo:
-            s = st[h]
-            s["iters"] += s["model"].n_iter()
-            s["nc"] += s["model"].k
-        host = torch.cat([cnt.double(), mses.double()]).cpu().numpy()  # the round's one sync
+            st[h]["nc"] += st[h]["model"].k
+        # the round's one sync: |U|, the stage MSE and the Lloyd iterations
+        host = torch.cat([cnt.double(), mses.double(), nits.double()]).cpu().numpy()
+        nt = len(todo)
         for j, h in enumerate(todo):
             s = st[h]
             s["pool"] = outs[j][:int(host[j])]
             s["size"] = int(host[j])
-            s["mse"].append(float(np.float32(host[len(todo) + j])))
+            s["mse"].append(float(np.float32(host[nt + j])))
+            m = s["model"]
+            s["iters"] += m.host_iters if m.host_iters is not None else int(host[2 * nt + j])
             s["rnd"] += 1
         live = [h for h in live if st[h]["size"] > 0 and not st[h]["flag"]]
         for h in list(live):
