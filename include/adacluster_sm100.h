@@ -225,10 +225,15 @@ int ac_get_assign_mode(void);
 /* centroid-update kernel selection (per calling thread): 0 = split-chain sums with
  * an exact f32 enclosure test (member-order chain per dimension only when
  * the enclosure straddles a rounding boundary) when the batch has csum/cabs
- * workspaces, 1 = always the member-order f64 chains (the default: its
- * small per-centre grid co-runs with the other Lloyd chains of a step and
- * measured faster end to end).  Both are bit-identical to np.add.reduceat
- * in member order.  Env AC_UPDATE_MODE overrides the default at load.      */
+ * workspaces, 1 = always the member-order f64 chains (its small per-centre
+ * grid co-runs with the other Lloyd chains of a step), 2 = the same
+ * enclosure-tested sums formed by streaming the rows in token order (no
+ * member-order gather; k·d·16 B of shared memory, else mode 0).  All are
+ * bit-identical to np.add.reduceat in member order.  Env AC_UPDATE_MODE
+ * overrides the default at load.                                           */
+#define AC_UPDATE_MODE_SPLIT 0
+#define AC_UPDATE_MODE_MEMBER 1
+#define AC_UPDATE_MODE_STREAM 2
 int ac_set_update_mode(int mode);
 int ac_get_update_mode(void);
 int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dtype,

@@ -1260,6 +1260,110 @@ k_ufin(const ac_cluster_problem* __restrict__ probs, int d, double tol) {
 }
 
 // ---------------------------------------------------------------------------
+// K4, streaming form of the split-chain sums (d = 64/128, k·d·16 B of shared
+// memory).  The enclosure test in k_ufin holds for ANY summation order, so
+// the member order (a gather through perm, one latency-bound walk per
+// cluster) is not needed to form Σx / Σ|x| / min|x|: each CTA streams a
+// contiguous range of rows in token order.  Warp w owns the labels
+// l ≡ w (mod kUsmWarps) and keeps their partial sums in shared memory
+// (no atomics: a (label, dim) slot has one writer); a warp loads only its
+// own rows, each row one coalesced 256/512-byte read.  At the end every
+// touched label is flushed into csum/cabs/clsb with global reductions, and
+// k_ufin finishes exactly as after k_usum.
+// ---------------------------------------------------------------------------
+constexpr int kUsmWarps = 16;
+constexpr int kUsmWin = 256;   // rows whose labels a warp scans per window
+constexpr int kUsmBatch = 8;   // own rows loaded per batch (in flight)
+
+__host__ __device__ inline size_t ustream_smem(int k, int d) {
+  return (size_t)k * d * 16 + sizeof(int) * (size_t)k;
+}
+
+template <int DPL, bool BF16>
+__global__ void __launch_bounds__(32 * kUsmWarps, 1)
+k_ustream(const ac_cluster_problem* __restrict__ probs, int d, int64_t chunk) {
+  extern __shared__ __align__(16) unsigned char ssm[];
+  const ac_cluster_problem& P = probs[blockIdx.y];
+  if (P.status[AC_ST_ACTIVE] == 0) return;
+  const int64_t n = P.n;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk;
+  if (r0 >= n) return;
+  const int64_t r1 = min(n, r0 + chunk);
+  const int k = P.k;
+  const int kd = k * d;
+  double* sacc = reinterpret_cast<double*>(ssm);   // [k][d]
+  float* sab = reinterpret_cast<float*>(sacc + kd);  // [k][d]
+  float* smn = sab + kd;                             // [k][d]
+  int* touched = reinterpret_cast<int*>(smn + kd);   // [k]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < kd; i += blockDim.x) { sacc[i] = 0.0; sab[i] = 0.f; smn[i] = INFINITY; }
+  for (int i = tid; i < k; i += blockDim.x) touched[i] = 0;
+  __syncthreads();
+  const int32_t* labels = P.labels;
+  // pending own rows: lane r holds the r-th (row, label) of the batch
+  int pend_row = 0, pend_lab = 0;
+  int npend = 0;
+  auto drain = [&]() {
+    float v[kUsmBatch][DPL];
+    int lb[kUsmBatch];
+#pragma unroll
+    for (int r = 0; r < kUsmBatch; ++r) {
+      const int row = __shfl_sync(0xffffffffu, pend_row, r);
+      lb[r] = __shfl_sync(0xffffffffu, pend_lab, r);
+      if (r < npend) load_row_part<DPL, BF16>(P.x, row, d, lane, v[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < kUsmBatch; ++r) {
+      if (r >= npend) break;
+      const int e = lb[r] * d + lane * DPL;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) {
+        const float a = fabsf(v[r][i]);
+        sacc[e + i] = __dadd_rn(sacc[e + i], (double)v[r][i]);
+        sab[e + i] = __fadd_rn(sab[e + i], a);
+        smn[e + i] = fminf(smn[e + i], a);
+      }
+    }
+    npend = 0;
+  };
+  for (int64_t base = r0; base < r1; base += kUsmWin) {
+    int lab[kUsmWin / 32];
+#pragma unroll
+    for (int j = 0; j < kUsmWin / 32; ++j) {
+      const int64_t r = base + 32 * j + lane;
+      lab[j] = r < r1 ? labels[r] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < kUsmWin / 32; ++j) {
+      unsigned m = __ballot_sync(0xffffffffu, lab[j] >= 0 && lab[j] % kUsmWarps == warp);
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        const int lb = __shfl_sync(0xffffffffu, lab[j], b);
+        if (lane == npend) { pend_row = (int)(base + 32 * j + b); pend_lab = lb; }
+        if (++npend == kUsmBatch) drain();
+      }
+    }
+  }
+  if (npend) drain();
+  // flush: every label this warp saw
+  for (int l = warp; l < k; l += kUsmWarps) {
+    const int e = l * d + lane * DPL;
+    bool any = false;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) any |= smn[e + i] != INFINITY;
+    if (!__any_sync(0xffffffffu, any)) continue;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      const int64_t g = (int64_t)l * d + lane * DPL + i;
+      atomicAdd(P.csum + g, sacc[e + i]);
+      atomicAdd(P.cabs + g, sab[e + i]);
+      atomicMin(P.clsb + g, __float_as_int(smn[e + i]));  // >= 0: int order == float order
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2: k-means++ seeding (clustering.py:78-91)
 // ---------------------------------------------------------------------------
 __global__ void k_kpp_init(const ac_cluster_problem* __restrict__ probs, int dtype, int d,
@@ -2042,7 +2146,7 @@ extern "C" int ac_set_assign_mode(int mode) {
 }
 extern "C" int ac_get_assign_mode(void) { return g_assign_mode; }
 extern "C" int ac_set_update_mode(int mode) {
-  if (mode < 0 || mode > 1) {
+  if (mode < AC_UPDATE_MODE_SPLIT || mode > AC_UPDATE_MODE_STREAM) {
     ac_host::set_error("ac_set_update_mode: bad mode %d", mode);
     return AC_ERR_PARAM;
   }
@@ -2075,8 +2179,32 @@ extern "C" int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dt
 static int usum_update_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
                             int64_t max_n, int max_k, double tol, cudaStream_t st) {
   const bool bf = dtype == AC_DTYPE_BF16;
-  const dim3 g1((unsigned)((max_n + kUsChunk * kUsWarps - 1) / (kUsChunk * kUsWarps)), nprob);
   const dim3 g2((unsigned)((max_k + 3) / 4), nprob);
+  const size_t ssm = ustream_smem(max_k, d);
+  if (g_update_mode == AC_UPDATE_MODE_STREAM && ssm <= 200 * 1024) {
+    // one wave: ~one (or, when the shared memory allows, two) CTA(s) per SM
+    // over all problems, each a contiguous multiple of kUsmWin rows
+    const int per_sm = ssm <= 100 * 1024 ? 2 : 1;
+    const int64_t ctas = (int64_t)ac_host::sm_count() * per_sm;
+    int64_t chunk = (max_n * nprob + ctas - 1) / ctas;
+    chunk = (chunk + kUsmWin - 1) / kUsmWin * kUsmWin;
+    const dim3 g1((unsigned)((max_n + chunk - 1) / chunk), nprob);
+    const void* fn = d == 64 ? (bf ? (const void*)k_ustream<2, true> : (const void*)k_ustream<2, false>)
+                             : (bf ? (const void*)k_ustream<4, true> : (const void*)k_ustream<4, false>);
+    int rc = set_smem(fn, ssm);
+    if (rc) return rc;
+    const int nt = 32 * kUsmWarps;
+    if (d == 64) {
+      if (bf) { k_ustream<2, true><<<g1, nt, ssm, st>>>(probs, d, chunk); k_ufin<2, true><<<g2, 128, 0, st>>>(probs, d, tol); }
+      else { k_ustream<2, false><<<g1, nt, ssm, st>>>(probs, d, chunk); k_ufin<2, false><<<g2, 128, 0, st>>>(probs, d, tol); }
+    } else {
+      if (bf) { k_ustream<4, true><<<g1, nt, ssm, st>>>(probs, d, chunk); k_ufin<4, true><<<g2, 128, 0, st>>>(probs, d, tol); }
+      else { k_ustream<4, false><<<g1, nt, ssm, st>>>(probs, d, chunk); k_ufin<4, false><<<g2, 128, 0, st>>>(probs, d, tol); }
+    }
+    AC_CHECK_LAUNCH("k_ustream/k_ufin");
+    return AC_OK;
+  }
+  const dim3 g1((unsigned)((max_n + kUsChunk * kUsWarps - 1) / (kUsChunk * kUsWarps)), nprob);
   if (d == 64) {
     if (bf) { k_usum<2, true><<<g1, 32 * kUsWarps, 0, st>>>(probs, d); k_ufin<2, true><<<g2, 128, 0, st>>>(probs, d, tol); }
     else { k_usum<2, false><<<g1, 32 * kUsWarps, 0, st>>>(probs, d); k_ufin<2, false><<<g2, 128, 0, st>>>(probs, d, tol); }
@@ -2092,7 +2220,7 @@ static int usum_update_impl(const ac_cluster_problem* probs, int nprob, int dtyp
 // the member-order chains the longest; bf16 points (128-byte rows) measured
 // faster with the member-order kernel.
 static bool usum_ok(const ac_cluster_problem* host_probs, int nprob, int dtype, int d) {
-  if (g_update_mode != 0 || !host_probs || !(d == 64 || d == 128)) return false;
+  if (g_update_mode == AC_UPDATE_MODE_MEMBER || !host_probs || !(d == 64 || d == 128)) return false;
   static const int bf_ok = getenv("AC_USUM_BF16") ? atoi(getenv("AC_USUM_BF16")) : 0;
   if (dtype != AC_DTYPE_F32 && !(dtype == AC_DTYPE_BF16 && bf_ok)) return false;
   for (int p = 0; p < nprob; ++p)

@@ -136,7 +136,8 @@ def test_tc_assign_lloyd_parity(gpu, oracle, d):
                                        ("bf16", 128, 128)])
 def test_split_chain_update_matches_member_order(gpu, dtype, d, k):
     """k_usum/k_ufin (split f64 chains + exact f32 enclosure test, member-order
-    fallback) give the same Lloyd run as the member-order chains, bit for bit."""
+    fallback) and k_ustream/k_ufin (the same sums streamed in token order)
+    give the same Lloyd run as the member-order chains, bit for bit."""
     from paper_2604_18348_b200 import _lib as L
     from paper_2604_18348_b200 import engine as E
     g = torch.Generator().manual_seed(d + k)
@@ -144,7 +145,7 @@ def test_split_chain_update_matches_member_order(gpu, dtype, d, k):
     xs = [(torch.randn(12000 + 777 * h, d, generator=g) * (1 + h)).to(tdt).cuda() for h in range(3)]
     runs = []
     prev = int(L.lib().ac_get_update_mode())
-    for mode in (0, 1):
+    for mode in (1, 0, 2):
         L.call("ac_set_update_mode", mode)
         try:
             ms = E.kmeans_batch(xs, [k] * 3, [1, 2, 3], 25, 1e-4)
@@ -152,10 +153,11 @@ def test_split_chain_update_matches_member_order(gpu, dtype, d, k):
             L.call("ac_set_update_mode", prev)
         torch.cuda.synchronize()
         runs.append([(m.centers.clone(), m.labels.clone(), m.n_iter()) for m in ms])
-    for (c0, l0, n0), (c1, l1, n1) in zip(*runs):
-        assert n0 == n1
-        assert torch.equal(l0, l1)
-        assert torch.equal(c0, c1)
+    for other in runs[1:]:
+        for (c0, l0, n0), (c1, l1, n1) in zip(runs[0], other):
+            assert n0 == n1
+            assert torch.equal(l0, l1)
+            assert torch.equal(c0, c1)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])

@@ -58,7 +58,8 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 for name, src, mode in [("token-order, member-order update", Q, 1),
                         ("token-order, split-chain update", Q, 0),
                         ("sorted, member-order update", Qs, 1),
-                        ("sorted, split-chain update", Qs, 0)]:
+                        ("sorted, split-chain update", Qs, 0),
+                        ("token-order, streamed update", Q, 2)]:
     run(src, mode)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
