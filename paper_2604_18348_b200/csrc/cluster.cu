@@ -1260,107 +1260,121 @@ k_ufin(const ac_cluster_problem* __restrict__ probs, int d, double tol) {
 }
 
 // ---------------------------------------------------------------------------
-// K4, streaming form of the split-chain sums (d = 64/128, k·d·16 B of shared
-// memory).  The enclosure test in k_ufin holds for ANY summation order, so
-// the member order (a gather through perm, one latency-bound walk per
-// cluster) is not needed to form Σx / Σ|x| / min|x|: each CTA streams a
-// contiguous range of rows in token order.  Warp w owns the labels
-// l ≡ w (mod kUsmWarps) and keeps their partial sums in shared memory
-// (no atomics: a (label, dim) slot has one writer); a warp loads only its
-// own rows, each row one coalesced 256/512-byte read.  At the end every
-// touched label is flushed into csum/cabs/clsb with global reductions, and
-// k_ufin finishes exactly as after k_usum.
+// K4, streaming form of the split-chain sums (d = 64/128).  The enclosure
+// test in k_ufin holds for ANY summation order, so the global member order
+// (a gather through perm whose longest cluster walk bounds the member-order
+// kernel) is not needed to form Σx and the bounds.  Each CTA owns a
+// contiguous range of at most kUsmChunk rows, counting-sorts the range by
+// label in shared memory (order inside a label is irrelevant), and its warps
+// take equal contiguous slices of that local order: f64 sums in registers
+// (lane = DPL consecutive dimensions), two batches of kUsmBatch rows in
+// flight (each row one coalesced 256/512-byte read from the CTA's range),
+// flushed into csum/cabs/clsb with global reductions at label boundaries.
+// The bounds are per lane rather than per dimension: Σ_rows max_i|x_i| over
+// the lane's DPL dimensions bounds Σ|x_t| of each of them and
+// min_rows min_i|x_i| bounds min|x_t| from below, so k_ufin's enclosure
+// stays valid (a few times wider; it still decides virtually every
+// dimension) and k_ufin finishes exactly as after k_usum.
 // ---------------------------------------------------------------------------
-constexpr int kUsmWarps = 16;
-constexpr int kUsmWin = 256;   // rows whose labels a warp scans per window
-constexpr int kUsmBatch = 8;   // own rows loaded per batch (in flight)
-
-__host__ __device__ inline size_t ustream_smem(int k, int d) {
-  return (size_t)k * d * 16 + sizeof(int) * (size_t)k;
-}
+constexpr int kUsmWarps = 8;
+constexpr int kUsmBatch = 8;     // rows per batch (two batches in flight per warp)
+constexpr int kUsmMaxK = 1024;   // labels a CTA can sort in shared memory
+constexpr int kUsmChunk = 4096;  // rows per CTA at most (12-bit row, 10-bit label packing)
+static int kUsmCtasPerSm = getenv("AC_USM_CTAS") ? atoi(getenv("AC_USM_CTAS")) : 4;
 
 template <int DPL, bool BF16>
-__global__ void __launch_bounds__(32 * kUsmWarps, 1)
+__global__ void __launch_bounds__(32 * kUsmWarps)
 k_ustream(const ac_cluster_problem* __restrict__ probs, int d, int64_t chunk) {
-  extern __shared__ __align__(16) unsigned char ssm[];
+  __shared__ int s_pos[kUsmMaxK];
+  __shared__ int s_sorted[kUsmChunk];  // label << 12 | row
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (P.status[AC_ST_ACTIVE] == 0) return;
   const int64_t n = P.n;
   const int64_t r0 = (int64_t)blockIdx.x * chunk;
   if (r0 >= n) return;
-  const int64_t r1 = min(n, r0 + chunk);
+  const int r1 = (int)min(n - r0, chunk);  // rows of this CTA: [r0, r0 + r1)
   const int k = P.k;
-  const int kd = k * d;
-  double* sacc = reinterpret_cast<double*>(ssm);   // [k][d]
-  float* sab = reinterpret_cast<float*>(sacc + kd);  // [k][d]
-  float* smn = sab + kd;                             // [k][d]
-  int* touched = reinterpret_cast<int*>(smn + kd);   // [k]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < kd; i += blockDim.x) { sacc[i] = 0.0; sab[i] = 0.f; smn[i] = INFINITY; }
-  for (int i = tid; i < k; i += blockDim.x) touched[i] = 0;
+  const int32_t* labels = P.labels + r0;
+  // counting sort of the range by label
+  for (int c = tid; c < k; c += blockDim.x) s_pos[c] = 0;
   __syncthreads();
-  const int32_t* labels = P.labels;
-  // pending own rows: lane r holds the r-th (row, label) of the batch
-  int pend_row = 0, pend_lab = 0;
-  int npend = 0;
-  auto drain = [&]() {
-    float v[kUsmBatch][DPL];
-    int lb[kUsmBatch];
+  for (int r = tid; r < r1; r += blockDim.x) atomicAdd(&s_pos[labels[r]], 1);
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the counts
+    int run = 0;
+    for (int c0 = 0; c0 < k; c0 += 32) {
+      const int c = c0 + lane;
+      const int v = c < k ? s_pos[c] : 0;
+      int inc = v;
 #pragma unroll
-    for (int r = 0; r < kUsmBatch; ++r) {
-      const int row = __shfl_sync(0xffffffffu, pend_row, r);
-      lb[r] = __shfl_sync(0xffffffffu, pend_lab, r);
-      if (r < npend) load_row_part<DPL, BF16>(P.x, row, d, lane, v[r]);
-    }
-#pragma unroll
-    for (int r = 0; r < kUsmBatch; ++r) {
-      if (r >= npend) break;
-      const int e = lb[r] * d + lane * DPL;
-#pragma unroll
-      for (int i = 0; i < DPL; ++i) {
-        const float a = fabsf(v[r][i]);
-        sacc[e + i] = __dadd_rn(sacc[e + i], (double)v[r][i]);
-        sab[e + i] = __fadd_rn(sab[e + i], a);
-        smn[e + i] = fminf(smn[e + i], a);
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
       }
-    }
-    npend = 0;
-  };
-  for (int64_t base = r0; base < r1; base += kUsmWin) {
-    int lab[kUsmWin / 32];
-#pragma unroll
-    for (int j = 0; j < kUsmWin / 32; ++j) {
-      const int64_t r = base + 32 * j + lane;
-      lab[j] = r < r1 ? labels[r] : -1;
-    }
-#pragma unroll
-    for (int j = 0; j < kUsmWin / 32; ++j) {
-      unsigned m = __ballot_sync(0xffffffffu, lab[j] >= 0 && lab[j] % kUsmWarps == warp);
-      while (m) {
-        const int b = __ffs(m) - 1;
-        m &= m - 1;
-        const int lb = __shfl_sync(0xffffffffu, lab[j], b);
-        if (lane == npend) { pend_row = (int)(base + 32 * j + b); pend_lab = lb; }
-        if (++npend == kUsmBatch) drain();
-      }
+      if (c < k) s_pos[c] = run + inc - v;
+      run += __shfl_sync(0xffffffffu, inc, 31);
     }
   }
-  if (npend) drain();
-  // flush: every label this warp saw
-  for (int l = warp; l < k; l += kUsmWarps) {
-    const int e = l * d + lane * DPL;
-    bool any = false;
+  __syncthreads();
+  for (int r = tid; r < r1; r += blockDim.x) {
+    const int l = labels[r];
+    s_sorted[atomicAdd(&s_pos[l], 1)] = (l << 12) | r;
+  }
+  __syncthreads();
+  // this warp's slice of the local order
+  const int per = (r1 + kUsmWarps - 1) / kUsmWarps;
+  const int p0 = warp * per, p1 = min(r1, p0 + per);
+  if (p0 >= p1) return;
+  const char* xb = reinterpret_cast<const char*>(P.x) + r0 * (int64_t)d * (BF16 ? 2 : 4);
+  double acc[DPL];
 #pragma unroll
-    for (int i = 0; i < DPL; ++i) any |= smn[e + i] != INFINITY;
-    if (!__any_sync(0xffffffffu, any)) continue;
+  for (int i = 0; i < DPL; ++i) acc[i] = 0.0;
+  float ab = 0.f, mn = INFINITY;
+  int cur = s_sorted[p0] >> 12;
+  auto flush = [&]() {
 #pragma unroll
     for (int i = 0; i < DPL; ++i) {
-      const int64_t g = (int64_t)l * d + lane * DPL + i;
-      atomicAdd(P.csum + g, sacc[e + i]);
-      atomicAdd(P.cabs + g, sab[e + i]);
-      atomicMin(P.clsb + g, __float_as_int(smn[e + i]));  // >= 0: int order == float order
+      const int64_t g = (int64_t)cur * d + lane * DPL + i;
+      atomicAdd(P.csum + g, acc[i]);
+      atomicAdd(P.cabs + g, ab);
+      atomicMin(P.clsb + g, __float_as_int(mn));  // >= 0: int order == float order
+      acc[i] = 0.0;
     }
+    ab = 0.f;
+    mn = INFINITY;
+  };
+  float va[kUsmBatch][DPL], vb[kUsmBatch][DPL];
+  auto load = [&](int q0, float (&v)[kUsmBatch][DPL]) {
+#pragma unroll
+    for (int r = 0; r < kUsmBatch; ++r)
+      if (q0 + r < p1) load_row_part<DPL, BF16>(xb, s_sorted[q0 + r] & 0xfff, d, lane, v[r]);
+  };
+  auto consume = [&](int q0, float (&v)[kUsmBatch][DPL]) {
+#pragma unroll
+    for (int r = 0; r < kUsmBatch; ++r) {
+      if (q0 + r >= p1) break;
+      const int l = s_sorted[q0 + r] >> 12;
+      if (l != cur) { flush(); cur = l; }
+      float mx = 0.f, mi = INFINITY;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) {
+        acc[i] = __dadd_rn(acc[i], (double)v[r][i]);
+        mx = fmaxf(mx, fabsf(v[r][i]));
+        mi = fminf(mi, fabsf(v[r][i]));
+      }
+      ab = __fadd_rn(ab, mx);
+      mn = fminf(mn, mi);
+    }
+  };
+  load(p0, va);
+  for (int q = p0; q < p1; q += 2 * kUsmBatch) {
+    load(q + kUsmBatch, vb);
+    consume(q, va);
+    load(q + 2 * kUsmBatch, va);
+    consume(q + kUsmBatch, vb);
   }
+  flush();
 }
 
 // ---------------------------------------------------------------------------
@@ -2180,19 +2194,14 @@ static int usum_update_impl(const ac_cluster_problem* probs, int nprob, int dtyp
                             int64_t max_n, int max_k, double tol, cudaStream_t st) {
   const bool bf = dtype == AC_DTYPE_BF16;
   const dim3 g2((unsigned)((max_k + 3) / 4), nprob);
-  const size_t ssm = ustream_smem(max_k, d);
-  if (g_update_mode == AC_UPDATE_MODE_STREAM && ssm <= 200 * 1024) {
-    // one wave: ~one (or, when the shared memory allows, two) CTA(s) per SM
-    // over all problems, each a contiguous multiple of kUsmWin rows
-    const int per_sm = ssm <= 100 * 1024 ? 2 : 1;
-    const int64_t ctas = (int64_t)ac_host::sm_count() * per_sm;
+  if (g_update_mode == AC_UPDATE_MODE_STREAM && max_k <= kUsmMaxK) {
+    // one wave of kUsmCtasPerSm CTAs per SM over all problems, each a
+    // contiguous multiple of 256 rows
+    const int64_t ctas = (int64_t)ac_host::sm_count() * kUsmCtasPerSm;
     int64_t chunk = (max_n * nprob + ctas - 1) / ctas;
-    chunk = (chunk + kUsmWin - 1) / kUsmWin * kUsmWin;
+    chunk = min((int64_t)kUsmChunk, (chunk + 255) / 256 * 256);
     const dim3 g1((unsigned)((max_n + chunk - 1) / chunk), nprob);
-    const void* fn = d == 64 ? (bf ? (const void*)k_ustream<2, true> : (const void*)k_ustream<2, false>)
-                             : (bf ? (const void*)k_ustream<4, true> : (const void*)k_ustream<4, false>);
-    int rc = set_smem(fn, ssm);
-    if (rc) return rc;
+    const size_t ssm = 0;
     const int nt = 32 * kUsmWarps;
     if (d == 64) {
       if (bf) { k_ustream<2, true><<<g1, nt, ssm, st>>>(probs, d, chunk); k_ufin<2, true><<<g2, 128, 0, st>>>(probs, d, tol); }
