@@ -227,13 +227,16 @@ int ac_get_assign_mode(void);
  * the enclosure straddles a rounding boundary) when the batch has csum/cabs
  * workspaces, 1 = always the member-order f64 chains (its small per-centre
  * grid co-runs with the other Lloyd chains of a step), 2 = the same
- * enclosure-tested sums formed by streaming the rows in token order (no
- * member-order gather; k·d·16 B of shared memory, else mode 0).  All are
- * bit-identical to np.add.reduceat in member order.  Env AC_UPDATE_MODE
- * overrides the default at load.                                           */
+ * enclosure-tested sums streamed over contiguous row ranges (every SM
+ * busy, no walk of a whole cluster by one warp; needs the csum/cabs/clsb
+ * workspaces and k <= 1024, else as mode 0), 3 = AUTO (the default): mode 2
+ * for batches with fewer than 512 centres in total (multi-stage planner
+ * rounds), mode 1 otherwise.  All are bit-identical to np.add.reduceat in
+ * member order.  Env AC_UPDATE_MODE overrides the default at load.        */
 #define AC_UPDATE_MODE_SPLIT 0
 #define AC_UPDATE_MODE_MEMBER 1
 #define AC_UPDATE_MODE_STREAM 2
+#define AC_UPDATE_MODE_AUTO 3
 int ac_set_update_mode(int mode);
 int ac_get_update_mode(void);
 int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dtype,

@@ -1952,7 +1952,8 @@ namespace {
 // GPUs or serve concurrent callers from several threads)
 thread_local int g_assign_mode = AC_ASSIGN_MODE_AUTO;
 // 0: split-chain update when eligible, 1: member-order chains (default)
-thread_local int g_update_mode = getenv("AC_UPDATE_MODE") ? atoi(getenv("AC_UPDATE_MODE")) : 1;
+thread_local int g_update_mode =
+    getenv("AC_UPDATE_MODE") ? atoi(getenv("AC_UPDATE_MODE")) : AC_UPDATE_MODE_AUTO;
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int set_smem(const void* fn, size_t bytes) {
@@ -2160,7 +2161,7 @@ extern "C" int ac_set_assign_mode(int mode) {
 }
 extern "C" int ac_get_assign_mode(void) { return g_assign_mode; }
 extern "C" int ac_set_update_mode(int mode) {
-  if (mode < AC_UPDATE_MODE_SPLIT || mode > AC_UPDATE_MODE_STREAM) {
+  if (mode < AC_UPDATE_MODE_SPLIT || mode > AC_UPDATE_MODE_AUTO) {
     ac_host::set_error("ac_set_update_mode: bad mode %d", mode);
     return AC_ERR_PARAM;
   }
@@ -2191,10 +2192,10 @@ extern "C" int ac_repair_sort(const ac_cluster_problem* probs, int nprob, int dt
 
 // split-chain update (k_usum + k_ufin) for a Lloyd iteration
 static int usum_update_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
-                            int64_t max_n, int max_k, double tol, cudaStream_t st) {
+                            int64_t max_n, int max_k, double tol, int mode, cudaStream_t st) {
   const bool bf = dtype == AC_DTYPE_BF16;
   const dim3 g2((unsigned)((max_k + 3) / 4), nprob);
-  if (g_update_mode == AC_UPDATE_MODE_STREAM && max_k <= kUsmMaxK) {
+  if (mode == AC_UPDATE_MODE_STREAM && max_k <= kUsmMaxK) {
     // one wave of kUsmCtasPerSm CTAs per SM over all problems, each a
     // contiguous multiple of 256 rows
     const int64_t ctas = (int64_t)ac_host::sm_count() * kUsmCtasPerSm;
@@ -2225,17 +2226,47 @@ static int usum_update_impl(const ac_cluster_problem* probs, int nprob, int dtyp
   return AC_OK;
 }
 
-// Used for f32 points: their 256/512-byte rows make the gather efficient and
-// the member-order chains the longest; bf16 points (128-byte rows) measured
-// faster with the member-order kernel.
+static bool usum_ws(const ac_cluster_problem* host_probs, int nprob, int d) {
+  if (!host_probs || !(d == 64 || d == 128)) return false;
+  for (int p = 0; p < nprob; ++p)
+    if (!host_probs[p].csum || !host_probs[p].cabs || !host_probs[p].clsb) return false;
+  return true;
+}
+
+// Mode 0 (split chains): used for f32 points, whose 256/512-byte rows make
+// the gather efficient and the member-order chains the longest; bf16 points
+// (128-byte rows) measured faster with the member-order kernel.
 static bool usum_ok(const ac_cluster_problem* host_probs, int nprob, int dtype, int d) {
-  if (g_update_mode == AC_UPDATE_MODE_MEMBER || !host_probs || !(d == 64 || d == 128)) return false;
+  if (g_update_mode != AC_UPDATE_MODE_SPLIT || !host_probs || !(d == 64 || d == 128)) return false;
   static const int bf_ok = getenv("AC_USUM_BF16") ? atoi(getenv("AC_USUM_BF16")) : 0;
   if (dtype != AC_DTYPE_F32 && !(dtype == AC_DTYPE_BF16 && bf_ok)) return false;
   for (int p = 0; p < nprob; ++p)
     if (!host_probs[p].csum || !host_probs[p].cabs || !host_probs[p].clsb) return false;
   return true;
 }
+
+// Update kernel of a Lloyd run.  The member-order kernel runs one warp per
+// centre on ceil(k / kUpdWarps) CTAs per problem: in a batch with few centres
+// in total (the multi-stage planner's rounds: one to a few heads, m_t = 8..100
+// centres) most SMs idle while single warps walk clusters of thousands of
+// members, so such batches take the streamed sums, which spread the rows
+// over every SM (one "mixed" C3 head's planner: 133 ms of member-order
+// updates over 925 launches).  Larger batches keep the default.
+static int update_mode_for(const ac_cluster_problem* host_probs, int nprob, int dtype, int d,
+                           int max_k) {
+  static const int small = getenv("AC_USM_SMALL") ? atoi(getenv("AC_USM_SMALL")) : 512;
+  const int mode = g_update_mode;
+  if (mode == AC_UPDATE_MODE_MEMBER) return mode;
+  if (mode == AC_UPDATE_MODE_AUTO) {
+    if ((int64_t)nprob * max_k < small && max_k <= kUsmMaxK && usum_ws(host_probs, nprob, d))
+      return AC_UPDATE_MODE_STREAM;
+    return AC_UPDATE_MODE_MEMBER;
+  }
+  if (mode == AC_UPDATE_MODE_STREAM && max_k <= kUsmMaxK && usum_ws(host_probs, nprob, d))
+    return mode;
+  return usum_ok(host_probs, nprob, dtype, d) ? AC_UPDATE_MODE_SPLIT : AC_UPDATE_MODE_MEMBER;
+}
+
 
 static int update_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d, int max_k,
                        double tol, int mode, float* const* outs, cudaStream_t st) {
@@ -2289,7 +2320,7 @@ static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int
   const int lo_flag = (!inertia && g_assign_mode != AC_ASSIGN_MODE_EXACT &&
                        ac_host::assign_tc_eligible(host_probs, nprob, dtype, d, 0, order))
                           ? AC_ASSIGN_LABELS_ONLY : 0;
-  const bool split_update = usum_ok(host_probs, nprob, dtype, d);
+  const int umode = update_mode_for(host_probs, nprob, dtype, d, max_k);
   int rc = prepare_impl(probs, nprob, dtype, d, max_n, max_k, (lflags & AC_LLOYD_PREPARED) != 0,
                         stream);
   if (rc) return rc;
@@ -2314,7 +2345,8 @@ static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int
       break;
     if ((rc = repair_sort_impl(probs, nprob, dtype, d, max_n, max_k, inertia ? it : -1, lo_flag, st)))
       break;
-    if (split_update) rc = usum_update_impl(probs, nprob, dtype, d, max_n, max_k, tol, st);
+    if (umode != AC_UPDATE_MODE_MEMBER)
+      rc = usum_update_impl(probs, nprob, dtype, d, max_n, max_k, tol, umode, st);
     else rc = update_impl(probs, nprob, dtype, d, max_k, tol, 0, nullptr, st);
     if (rc) break;
     if (pinned && (it + 1) % poll_every == 0 && it + 1 < max_iter) {

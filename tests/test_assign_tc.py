@@ -145,7 +145,7 @@ def test_split_chain_update_matches_member_order(gpu, dtype, d, k):
     xs = [(torch.randn(12000 + 777 * h, d, generator=g) * (1 + h)).to(tdt).cuda() for h in range(3)]
     runs = []
     prev = int(L.lib().ac_get_update_mode())
-    for mode in (1, 0, 2):
+    for mode in (1, 0, 2, 3):
         L.call("ac_set_update_mode", mode)
         try:
             ms = E.kmeans_batch(xs, [k] * 3, [1, 2, 3], 25, 1e-4)
