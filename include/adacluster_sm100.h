@@ -369,6 +369,12 @@ int ac_build_q_layout(const void* q, int dtype, int d, int64_t L, int heads,
  * ac_build_q_layout: 256 for the two-tile tcgen05 kernel (bf16, d = 64),
  * else 128                                                                 */
 int ac_attention_item_rows(int dtype, int d);
+/* reorder `nitems` work items in place, longest first (Q tiles x K/V tiles of
+ * their runs): the attention launch then issues them as greedy LPT list
+ * scheduling.  Items write disjoint output rows, so results do not depend
+ * on the order.  scratch: nitems * sizeof(ac_attn_item) bytes.             */
+int ac_order_items(ac_attn_item* items, int nitems, const int32_t* runs,
+                   ac_attn_item* scratch, void* stream);
 
 /* ---- K13/K14 block-sparse attention --------------------------------------
  * One work item = one tile of <= 128 query rows of one query cluster of one

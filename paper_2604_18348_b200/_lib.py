@@ -98,6 +98,7 @@ _SIGS = {
     "ac_build_q_layout": [_P, _I, _I, _I64, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P, _I64,
                           _P, _I, _I, _P],
     "ac_attention_item_rows": [_I, _I],
+    "ac_order_items": [_P, _I, _P, _P, _P],
     "ac_sparse_attention": [_P, _I64, _P, _P, _P, _I, _I, _I64, _I, _P, _I, _P, _F, _P, _I, _P],
     "ac_sparse_attention_fa4": [_P, _I64, _P, _P, _P, _I, _I64, _I, _P, _I, _P, _F, _P, _I, _P],
     "ac_sparse_attention_fa4_d128": [_P, _I64, _P, _P, _P, _I, _I64, _I, _P, _I, _P, _F, _P, _I, _P],

@@ -271,6 +271,72 @@ int launch_simt(const void* q, const int32_t* qidx, const void* k, const void* v
   return AC_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Work-item order for the attention launch: longest first.  The attention
+// kernels take one item per CTA in blockIdx order, which the hardware
+// dispatches roughly in order as SMs free up, so issuing the items by
+// descending cost (Q tiles x K/V tiles of its runs) is greedy LPT list
+// scheduling: the last CTAs to start are the shortest, which shortens the
+// tail of the launch.  Items write disjoint output rows, so the order does
+// not change any result.  One CTA: cost buckets (descending), counting-sort
+// scatter into `scratch`, copy back.
+// ---------------------------------------------------------------------------
+constexpr int kOrdBuckets = 4096;
+
+AC_DEV int item_cost(const ac_attn_item& m, const int32_t* runs) {
+  if (m.q_rows <= 0) return 0;
+  const int32_t* r = runs + 2 * (int64_t)m.run0;
+  int tiles = 0;
+  for (int i = 0; i < m.nruns; ++i) tiles += (r[2 * i + 1] - r[2 * i] + 127) / 128;
+  return ((m.q_rows + 127) / 128) * (tiles + 2);  // +2: per-item prologue / epilogue
+}
+
+__global__ void __launch_bounds__(1024)
+k_order_items(ac_attn_item* __restrict__ items, int nitems, const int32_t* __restrict__ runs,
+              ac_attn_item* __restrict__ scratch) {
+  __shared__ int hist[kOrdBuckets];
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b = tid; b < kOrdBuckets; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  auto key = [&](int i) {  // descending cost
+    return kOrdBuckets - 1 - min(item_cost(items[i], runs), kOrdBuckets - 1);
+  };
+  for (int i = tid; i < nitems; i += blockDim.x) atomicAdd(&hist[key(i)], 1);
+  __syncthreads();
+  // exclusive scan: 4 buckets per thread, then a block scan of the thread sums
+  constexpr int kPer = kOrdBuckets / 1024;
+  int loc[kPer], tot = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) { loc[j] = hist[tid * kPer + j]; tot += loc[j]; }
+  int inc = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int w = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    wsum[lane] = w;
+  }
+  __syncthreads();
+  int run = (warp ? wsum[warp - 1] : 0) + inc - tot;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) { hist[tid * kPer + j] = run; run += loc[j]; }
+  __syncthreads();
+  for (int i = tid; i < nitems; i += blockDim.x) scratch[atomicAdd(&hist[key(i)], 1)] = items[i];
+  __syncthreads();
+  for (int i = tid; i < nitems; i += blockDim.x) items[i] = scratch[i];
+}
+
 }  // namespace ac
 
 using namespace ac;
@@ -362,4 +428,16 @@ extern "C" int ac_sparse_attention_simt(const void* q, const int32_t* qidx, cons
       ac_host::set_error("attention: head_dim %d unsupported (16/32/64/128; pad smaller dims)", d);
       return AC_ERR_DIM;
   }
+}
+
+extern "C" int ac_order_items(ac_attn_item* items, int nitems, const int32_t* runs,
+                              ac_attn_item* scratch, void* stream) {
+  if (nitems <= 0) return AC_OK;
+  if (!items || !runs || !scratch) {
+    ac_host::set_error("ac_order_items: null pointer");
+    return AC_ERR_PARAM;
+  }
+  k_order_items<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(items, nitems, runs, scratch);
+  AC_CHECK_LAUNCH("k_order_items");
+  return AC_OK;
 }

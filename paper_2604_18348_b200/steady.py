@@ -57,7 +57,12 @@ class Workspace:
         self.qidx = torch.empty(H * self.qp_cap + H * gq, dtype=I32, device=dev)
         self.items = torch.empty(H * self.item_cap * L.ITEM_DTYPE.itemsize, dtype=torch.uint8,
                                  device=dev)
+        self.items_scratch = torch.empty_like(self.items)  # ac_order_items
         self.out = torch.empty((H, Ln, D), dtype=odt, device=dev)
+
+
+# issue the attention work items longest first (AC_ITEM_ORDER=0: layout order)
+_ORDER_ITEMS = os.environ.get("AC_ITEM_ORDER", "1") != "0"
 
 
 class SteadyStep:
@@ -161,6 +166,7 @@ class SteadyStep:
         self.qp_cap, self.item_cap = ws.qp_cap, ws.item_cap
         self.item_rows = int(L.lib().ac_attention_item_rows(self.dt, D))
         self.qp, self.qidx, self.items, self.out = ws.qp, ws.qidx, ws.items, ws.out
+        self.items_scratch = ws.items_scratch
         self.odt = L.dtype_code(self.out) if self.out_dtype != F32 else L.DTYPE_F32
         self.scale = float(1.0 / math.sqrt(D))
         self.graph = None
@@ -359,6 +365,10 @@ class SteadyStep:
         """Attention of the work items of heads [h0, h1) (layout built for all
         heads: items carry absolute head indices), current stream."""
         isz = L.ITEM_DTYPE.itemsize
+        if _ORDER_ITEMS:  # longest items first (LPT issue order)
+            L.call("ac_order_items", self.items.data_ptr() + h0 * self.item_cap * isz,
+                   (h1 - h0) * self.item_cap, self.runs.data_ptr(), self.items_scratch.data_ptr(),
+                   L.stream_ptr())
         L.call("ac_sparse_attention", self.qp.data_ptr(), self.H * self.qp_cap, self.qidx.data_ptr(),
                self.kp.data_ptr(), self.vp.data_ptr(), self.dt, self.D, self.L, self.H,
                self.items.data_ptr() + h0 * self.item_cap * isz, (h1 - h0) * self.item_cap,
