@@ -22,7 +22,7 @@ def _cost(it, runs):
 def test_order_items_is_a_longest_first_permutation(gpu, n):
     from paper_2604_18348_b200 import _lib as L
     rng = np.random.default_rng(n)
-    nruns_tot = 4 * n
+    nruns_tot = 4 * n + 4
     starts = rng.integers(0, 100000, size=nruns_tot)
     lens = rng.integers(1, 2000, size=nruns_tot)
     runs = np.stack([starts, starts + lens], 1).reshape(-1).astype(np.int32)
