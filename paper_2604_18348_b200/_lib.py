@@ -7,8 +7,10 @@ map onto the reference exception classes (errors.py:8-29).
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import functools
+import os
 from pathlib import Path
 
 import numpy as np
@@ -81,6 +83,8 @@ _SIGS = {
     "ac_get_assign_mode": [],
     "ac_set_update_mode": [_I],
     "ac_get_update_mode": [],
+    "ac_set_pdl": [_I],
+    "ac_get_pdl": [],
     "ac_repair_sort": [_P, _I, _I, _I, _I64, _I, _I, _I, _P],
     "ac_segment_mean": [_P, _I, _I, _I, _I, _P, _P],
     "ac_sort_by_label": [_P, _I, _I64, _I, _P],
@@ -139,6 +143,24 @@ def check(rc: int, what: str = "") -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(lib(), name)(*args), name)
+
+
+@contextlib.contextmanager
+def pdl(on: bool = True):
+    """Programmatic dependent launch of the Lloyd-chain kernels enqueued (or
+    captured) inside the block, on this thread (ac_set_pdl)."""
+    prev = int(lib().ac_get_pdl())
+    call("ac_set_pdl", int(bool(on)))
+    try:
+        yield
+    finally:
+        call("ac_set_pdl", prev)
+
+
+# where the engine turns it on: lone chains of small launches (steady steps
+# of at most this many rows per layer, the multi-stage planner's rounds)
+PDL_STEADY_ROWS = int(os.environ.get("AC_PDL_STEADY_ROWS", "200000"))
+PDL_PLANNER = os.environ.get("AC_PDL_PLANNER", "1") != "0"
 
 
 @functools.lru_cache(maxsize=None)

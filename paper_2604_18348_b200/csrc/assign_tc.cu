@@ -232,6 +232,8 @@ AC_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 template <int DIM, int NWG>
 __global__ void __launch_bounds__(NWG == 2 ? 320 : (NWG == 3 ? 512 : 576), 1)
 k_assign_tc(const __grid_constant__ Params prm, const ac_cluster_problem* __restrict__ probs) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int THREADS = threads_for(NWG);
   constexpr int KB = DIM / 64;           // SW128 K-atoms per row
   constexpr int PL_BYTES = KB * ATOM;    // one bf16 plane of a tile
@@ -702,14 +704,14 @@ int assign_tc_launch(const ac_cluster_problem* probs, const ac_cluster_problem* 
     static const int env_wg = getenv("AC_ASG_WG") ? atoi(getenv("AC_ASG_WG")) : 0;
     const int nwg = (env_wg >= 2 && env_wg <= 4) ? env_wg : (d == 64 ? 4 : 3);
     if (nwg == 4) {
-      if (d == 64) k_assign_tc<64, 4><<<grid, threads_for(4), prm.lay.smem, st>>>(prm, probs + p0);
-      else k_assign_tc<128, 4><<<grid, threads_for(4), prm.lay.smem, st>>>(prm, probs + p0);
+      if (d == 64) ac_host::launch_pdl(k_assign_tc<64, 4>, dim3(grid), dim3(threads_for(4)), prm.lay.smem, st, prm, probs + p0);
+      else ac_host::launch_pdl(k_assign_tc<128, 4>, dim3(grid), dim3(threads_for(4)), prm.lay.smem, st, prm, probs + p0);
     } else if (nwg == 2) {
-      if (d == 64) k_assign_tc<64, 2><<<grid, threads_for(2), prm.lay.smem, st>>>(prm, probs + p0);
-      else k_assign_tc<128, 2><<<grid, threads_for(2), prm.lay.smem, st>>>(prm, probs + p0);
+      if (d == 64) ac_host::launch_pdl(k_assign_tc<64, 2>, dim3(grid), dim3(threads_for(2)), prm.lay.smem, st, prm, probs + p0);
+      else ac_host::launch_pdl(k_assign_tc<128, 2>, dim3(grid), dim3(threads_for(2)), prm.lay.smem, st, prm, probs + p0);
     } else {
-      if (d == 64) k_assign_tc<64, 3><<<grid, threads_for(3), prm.lay.smem, st>>>(prm, probs + p0);
-      else k_assign_tc<128, 3><<<grid, threads_for(3), prm.lay.smem, st>>>(prm, probs + p0);
+      if (d == 64) ac_host::launch_pdl(k_assign_tc<64, 3>, dim3(grid), dim3(threads_for(3)), prm.lay.smem, st, prm, probs + p0);
+      else ac_host::launch_pdl(k_assign_tc<128, 3>, dim3(grid), dim3(threads_for(3)), prm.lay.smem, st, prm, probs + p0);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return check_cuda(e, "k_assign_tc");

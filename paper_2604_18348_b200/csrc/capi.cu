@@ -49,6 +49,12 @@ int func_smem(const void* fn, int bytes, const char* what) {
   return AC_OK;
 }
 
+// per calling thread, like the assign/update modes (a CUDA graph keeps the
+// attribute its kernels were captured with); env AC_PDL sets the default
+static int pdl_default() { return getenv("AC_PDL") ? atoi(getenv("AC_PDL")) : 0; }
+thread_local int g_pdl = pdl_default();
+bool pdl_on() { return g_pdl != 0; }
+
 int sm_count() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
@@ -315,3 +321,9 @@ extern "C" int64_t ac_workspace_bytes(int op, const int64_t* dims, int ndims, in
   ac_host::set_error("ac_workspace_bytes: unknown op %d", op);
   return -1;
 }
+
+extern "C" int ac_set_pdl(int on) {
+  ac_host::g_pdl = on != 0;
+  return AC_OK;
+}
+extern "C" int ac_get_pdl(void) { return ac_host::g_pdl; }

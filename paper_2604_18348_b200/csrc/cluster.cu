@@ -271,6 +271,8 @@ k_problem_xx_v(const ac_cluster_problem* __restrict__ probs, int dtype) {
 // center squared norms cc[c] for problem blockIdx.y
 __global__ void k_center_sqnorm(const ac_cluster_problem* __restrict__ probs, int d,
                                 int c_lo) {
+  pdl_wait();
+  pdl_trigger();
   const ac_cluster_problem& P = probs[blockIdx.y];
   const int c = c_lo + blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= P.k) return;
@@ -514,6 +516,8 @@ __global__ void k_assign_generic(const ac_cluster_problem* __restrict__ probs, i
 
 // per-tile label histogram from existing labels (sort without re-assigning)
 __global__ void k_tile_hist(const ac_cluster_problem* __restrict__ probs, int kcap) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) int thsm[];
   const ac_cluster_problem& P = probs[blockIdx.y];
   const int64_t row0 = (int64_t)blockIdx.x * kAsgBM;
@@ -537,6 +541,8 @@ __global__ void k_tile_hist(const ac_cluster_problem* __restrict__ probs, int kc
 //   scatter: perm[starts[c] + base[tile][c] + rank-in-tile] = row
 // ---------------------------------------------------------------------------
 __global__ void k_hist_scan(const ac_cluster_problem* __restrict__ probs, int flags) {
+  pdl_wait();
+  pdl_trigger();
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (!(flags & AC_ASSIGN_ALL) && P.status[AC_ST_ACTIVE] == 0) return;
   const int k = P.k;
@@ -565,6 +571,8 @@ __global__ void k_hist_scan(const ac_cluster_problem* __restrict__ probs, int fl
 // One CTA (1024 threads) per problem.  `iter` < 0 skips the inertia entry.
 __global__ void __launch_bounds__(1024)
 k_post(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int iter, int flags) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char psm[];
   const ac_cluster_problem& P = probs[blockIdx.x];
   if (!(flags & AC_ASSIGN_ALL) && P.status[AC_ST_ACTIVE] == 0) return;
@@ -686,6 +694,8 @@ k_post(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int iter,
 }
 
 __global__ void k_scatter(const ac_cluster_problem* __restrict__ probs, int flags) {
+  pdl_wait();
+  pdl_trigger();
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (!(flags & AC_ASSIGN_ALL) && P.status[AC_ST_ACTIVE] == 0) return;
   const int64_t row0 = (int64_t)blockIdx.x * kAsgBM;
@@ -742,6 +752,8 @@ __host__ __device__ inline size_t update_smem_bytes(int d, int dtype) {
 __global__ void __launch_bounds__(256)
 k_update(const ac_cluster_problem* __restrict__ probs, int dtype, int d, double tol,
          int mode /*0 = lloyd update, 1 = segment mean into out*/, float* const* outs) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char usm[];
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (mode == 0 && P.status[AC_ST_ACTIVE] == 0) return;
@@ -892,6 +904,8 @@ template <int DPL, bool BF16>
 __global__ void __launch_bounds__(32 * kUpdWarps)
 k_update_w(const ac_cluster_problem* __restrict__ probs, int d, double tol, int mode,
            float* const* outs) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char wsm[];
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (mode == 0 && P.status[AC_ST_ACTIVE] == 0) return;
@@ -1087,6 +1101,8 @@ AC_DEV void load_row_part(const void* x, int64_t row, int d, int lane, float (&v
 template <int DPL, bool BF16>
 __global__ void __launch_bounds__(32 * kUsWarps)
 k_usum(const ac_cluster_problem* __restrict__ probs, int d) {
+  pdl_wait();
+  pdl_trigger();
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (P.status[AC_ST_ACTIVE] == 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1156,6 +1172,8 @@ k_usum(const ac_cluster_problem* __restrict__ probs, int d) {
 template <int DPL, bool BF16>
 __global__ void __launch_bounds__(128)
 k_ufin(const ac_cluster_problem* __restrict__ probs, int d, double tol) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float s_sq[4][2][256];
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (P.status[AC_ST_ACTIVE] == 0) return;
@@ -1285,6 +1303,8 @@ static int kUsmCtasPerSm = getenv("AC_USM_CTAS") ? atoi(getenv("AC_USM_CTAS")) :
 template <int DPL, bool BF16>
 __global__ void __launch_bounds__(32 * kUsmWarps)
 k_ustream(const ac_cluster_problem* __restrict__ probs, int d, int64_t chunk) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_pos[kUsmMaxK];
   __shared__ int s_sorted[kUsmChunk];  // label << 12 | row
   const ac_cluster_problem& P = probs[blockIdx.y];
@@ -2089,7 +2109,7 @@ static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
     return AC_ERR_PARAM;
   }
   if (tc_ok && mode != AC_ASSIGN_MODE_EXACT) {
-    if (!cc_valid) k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
+    if (!cc_valid) ac_host::launch_pdl(k_center_sqnorm, dim3(dim3((max_k + 127) / 128, nprob)), dim3(128), 0, st, probs, d, c_lo);
     AC_CHECK_LAUNCH("k_center_sqnorm");
     return ac_host::assign_tc_launch(probs, host_probs, nprob, dtype, d, c_lo, flags, st);
   }
@@ -2099,7 +2119,7 @@ static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
   {
     const bool ok = chunk_ok;
     if (ok) {
-      if (!cc_valid) k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, 0);
+      if (!cc_valid) ac_host::launch_pdl(k_center_sqnorm, dim3(dim3((max_k + 127) / 128, nprob)), dim3(128), 0, st, probs, d, 0);
       AC_CHECK_LAUNCH("k_center_sqnorm");
       const int base = (flags & ~AC_ASSIGN_LABELS_ONLY) | ac::kAsgNoHist;
       for (int c0 = 0; c0 < max_k; c0 += ac::kAsgTcChunk) {
@@ -2114,7 +2134,7 @@ static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
       const size_t hsm = sizeof(int) * (size_t)(max_k + 4);
       int rc = set_smem((const void*)k_tile_hist, hsm);
       if (rc) return rc;
-      k_tile_hist<<<dim3(tiles, nprob), kAsgBM, hsm, st>>>(probs, max_k);
+      ac_host::launch_pdl(k_tile_hist, dim3(dim3(tiles, nprob)), dim3(kAsgBM), hsm, st, probs, max_k);
       AC_CHECK_LAUNCH("k_tile_hist");
       return AC_OK;
     }
@@ -2123,13 +2143,13 @@ static int assign_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
     const size_t smem = assign_smem_bytes(d, max_k);
     int rc = set_smem((const void*)k_assign_seq, smem);
     if (rc) return rc;
-    if (!cc_valid) k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
+    if (!cc_valid) ac_host::launch_pdl(k_center_sqnorm, dim3(dim3((max_k + 127) / 128, nprob)), dim3(128), 0, st, probs, d, c_lo);
     k_assign_seq<<<dim3(tiles, nprob), 256, smem, st>>>(probs, dtype, d, c_lo, flags, max_k);
   } else {
     const size_t smem = sizeof(int) * (size_t)(max_k + 4);
     int rc = set_smem((const void*)k_assign_generic, smem);
     if (rc) return rc;
-    if (!cc_valid) k_center_sqnorm<<<dim3((max_k + 127) / 128, nprob), 128, 0, st>>>(probs, d, c_lo);
+    if (!cc_valid) ac_host::launch_pdl(k_center_sqnorm, dim3(dim3((max_k + 127) / 128, nprob)), dim3(128), 0, st, probs, d, c_lo);
     k_assign_generic<<<dim3(tiles, nprob), kAsgBM, smem, st>>>(probs, dtype, d, c_lo, flags, max_k);
   }
   AC_CHECK_LAUNCH("ac_assign");
@@ -2174,12 +2194,12 @@ extern "C" int ac_get_update_mode(void) { return g_update_mode; }
 static int repair_sort_impl(const ac_cluster_problem* probs, int nprob, int dtype, int d,
                             int64_t max_n, int max_k, int iter, int flags, cudaStream_t st) {
   const unsigned tiles = (unsigned)((max_n + kAsgBM - 1) / kAsgBM);
-  k_hist_scan<<<dim3((max_k + 7) / 8, nprob), 256, 0, st>>>(probs, flags);
+  ac_host::launch_pdl(k_hist_scan, dim3(dim3((max_k + 7) / 8, nprob)), dim3(256), 0, st, probs, flags);
   const size_t psm = plan_vals_bytes(max_n, sizeof(float));
   int rc = set_smem((const void*)k_post, psm);
   if (rc) return rc;
-  k_post<<<nprob, 1024, psm, st>>>(probs, dtype, d, iter, flags);
-  k_scatter<<<dim3(tiles, nprob), kAsgBM, 0, st>>>(probs, flags);
+  ac_host::launch_pdl(k_post, dim3(nprob), dim3(1024), psm, st, probs, dtype, d, iter, flags);
+  ac_host::launch_pdl(k_scatter, dim3(dim3(tiles, nprob)), dim3(kAsgBM), 0, st, probs, flags);
   AC_CHECK_LAUNCH("ac_repair_sort");
   return AC_OK;
 }
@@ -2205,22 +2225,22 @@ static int usum_update_impl(const ac_cluster_problem* probs, int nprob, int dtyp
     const size_t ssm = 0;
     const int nt = 32 * kUsmWarps;
     if (d == 64) {
-      if (bf) { k_ustream<2, true><<<g1, nt, ssm, st>>>(probs, d, chunk); k_ufin<2, true><<<g2, 128, 0, st>>>(probs, d, tol); }
-      else { k_ustream<2, false><<<g1, nt, ssm, st>>>(probs, d, chunk); k_ufin<2, false><<<g2, 128, 0, st>>>(probs, d, tol); }
+      if (bf) { ac_host::launch_pdl(k_ustream<2, true>, dim3(g1), dim3(nt), ssm, st, probs, d, chunk); ac_host::launch_pdl(k_ufin<2, true>, dim3(g2), dim3(128), 0, st, probs, d, tol); }
+      else { ac_host::launch_pdl(k_ustream<2, false>, dim3(g1), dim3(nt), ssm, st, probs, d, chunk); ac_host::launch_pdl(k_ufin<2, false>, dim3(g2), dim3(128), 0, st, probs, d, tol); }
     } else {
-      if (bf) { k_ustream<4, true><<<g1, nt, ssm, st>>>(probs, d, chunk); k_ufin<4, true><<<g2, 128, 0, st>>>(probs, d, tol); }
-      else { k_ustream<4, false><<<g1, nt, ssm, st>>>(probs, d, chunk); k_ufin<4, false><<<g2, 128, 0, st>>>(probs, d, tol); }
+      if (bf) { ac_host::launch_pdl(k_ustream<4, true>, dim3(g1), dim3(nt), ssm, st, probs, d, chunk); ac_host::launch_pdl(k_ufin<4, true>, dim3(g2), dim3(128), 0, st, probs, d, tol); }
+      else { ac_host::launch_pdl(k_ustream<4, false>, dim3(g1), dim3(nt), ssm, st, probs, d, chunk); ac_host::launch_pdl(k_ufin<4, false>, dim3(g2), dim3(128), 0, st, probs, d, tol); }
     }
     AC_CHECK_LAUNCH("k_ustream/k_ufin");
     return AC_OK;
   }
   const dim3 g1((unsigned)((max_n + kUsChunk * kUsWarps - 1) / (kUsChunk * kUsWarps)), nprob);
   if (d == 64) {
-    if (bf) { k_usum<2, true><<<g1, 32 * kUsWarps, 0, st>>>(probs, d); k_ufin<2, true><<<g2, 128, 0, st>>>(probs, d, tol); }
-    else { k_usum<2, false><<<g1, 32 * kUsWarps, 0, st>>>(probs, d); k_ufin<2, false><<<g2, 128, 0, st>>>(probs, d, tol); }
+    if (bf) { ac_host::launch_pdl(k_usum<2, true>, dim3(g1), dim3(32 * kUsWarps), 0, st, probs, d); ac_host::launch_pdl(k_ufin<2, true>, dim3(g2), dim3(128), 0, st, probs, d, tol); }
+    else { ac_host::launch_pdl(k_usum<2, false>, dim3(g1), dim3(32 * kUsWarps), 0, st, probs, d); ac_host::launch_pdl(k_ufin<2, false>, dim3(g2), dim3(128), 0, st, probs, d, tol); }
   } else {
-    if (bf) { k_usum<4, true><<<g1, 32 * kUsWarps, 0, st>>>(probs, d); k_ufin<4, true><<<g2, 128, 0, st>>>(probs, d, tol); }
-    else { k_usum<4, false><<<g1, 32 * kUsWarps, 0, st>>>(probs, d); k_ufin<4, false><<<g2, 128, 0, st>>>(probs, d, tol); }
+    if (bf) { ac_host::launch_pdl(k_usum<4, true>, dim3(g1), dim3(32 * kUsWarps), 0, st, probs, d); ac_host::launch_pdl(k_ufin<4, true>, dim3(g2), dim3(128), 0, st, probs, d, tol); }
+    else { ac_host::launch_pdl(k_usum<4, false>, dim3(g1), dim3(32 * kUsWarps), 0, st, probs, d); ac_host::launch_pdl(k_ufin<4, false>, dim3(g2), dim3(128), 0, st, probs, d, tol); }
   }
   AC_CHECK_LAUNCH("k_usum/k_ufin");
   return AC_OK;
@@ -2280,11 +2300,11 @@ static int update_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
     int rc = set_smem(fn, wsmem);
     if (rc) return rc;
     if (d == 64) {
-      if (bf) k_update_w<2, true><<<grid, 32 * kUpdWarps, wsmem, st>>>(probs, d, tol, mode, outs);
-      else k_update_w<2, false><<<grid, 32 * kUpdWarps, wsmem, st>>>(probs, d, tol, mode, outs);
+      if (bf) ac_host::launch_pdl(k_update_w<2, true>, dim3(grid), dim3(32 * kUpdWarps), wsmem, st, probs, d, tol, mode, outs);
+      else ac_host::launch_pdl(k_update_w<2, false>, dim3(grid), dim3(32 * kUpdWarps), wsmem, st, probs, d, tol, mode, outs);
     } else {
-      if (bf) k_update_w<4, true><<<grid, 32 * kUpdWarps, wsmem, st>>>(probs, d, tol, mode, outs);
-      else k_update_w<4, false><<<grid, 32 * kUpdWarps, wsmem, st>>>(probs, d, tol, mode, outs);
+      if (bf) ac_host::launch_pdl(k_update_w<4, true>, dim3(grid), dim3(32 * kUpdWarps), wsmem, st, probs, d, tol, mode, outs);
+      else ac_host::launch_pdl(k_update_w<4, false>, dim3(grid), dim3(32 * kUpdWarps), wsmem, st, probs, d, tol, mode, outs);
     }
     AC_CHECK_LAUNCH("k_update_w");
     return AC_OK;
@@ -2292,7 +2312,7 @@ static int update_impl(const ac_cluster_problem* probs, int nprob, int dtype, in
   const size_t smem = update_smem_bytes(d, dtype);
   int rc = set_smem((const void*)k_update, smem);
   if (rc) return rc;
-  k_update<<<dim3(max_k, nprob), d <= 128 ? 128 : 256, smem, st>>>(probs, dtype, d, tol, mode, outs);
+  ac_host::launch_pdl(k_update, dim3(dim3(max_k, nprob)), dim3(d <= 128 ? 128 : 256), smem, st, probs, dtype, d, tol, mode, outs);
   AC_CHECK_LAUNCH("k_update");
   return AC_OK;
 }

@@ -107,6 +107,17 @@ AC_DEV void argmax_merge(float& bd, int64_t& bi, float od, int64_t oi) {
   if (od > bd || (od == bd && oi < bi)) { bd = od; bi = oi; }
 }
 
+// Programmatic dependent launch.  A kernel of a Lloyd chain that may be
+// launched with the programmatic-serialisation attribute starts with
+// pdl_wait() (griddepcontrol.wait: returns once the previous kernel of the
+// stream has completed and its memory is visible; a no-op for a normal
+// launch), so nothing it reads can be stale; pdl_trigger() then lets the
+// next kernel of the stream be scheduled while this one runs, which hides
+// the launch and ramp of the ~125 dependent launches of a 25-iteration
+// chain behind the tails of their predecessors.
+AC_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+AC_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 }  // namespace ac
 
 // host-side error reporting shared by every translation unit
@@ -120,6 +131,27 @@ int check_cuda(cudaError_t e, const char* what);
 int func_smem(const void* fn, int bytes, const char* what);
 // multiprocessor count of the current device (cached per device)
 int sm_count();
+// programmatic dependent launches of the Lloyd-chain kernels (env AC_PDL, default on)
+bool pdl_on();
+
+// kern<<<grid, block, smem, st>>>(args...) with the programmatic stream
+// serialisation attribute when pdl_on(): the kernel must begin with
+// ac::pdl_wait()
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 }  // namespace ac_host
 
 #define AC_CHECK_LAUNCH(what)                                                   \

@@ -587,6 +587,40 @@ def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0:
             base.tau = float(taus[h])
             base.host_iters = base.n_iter()
             results[h] = base
+    with L.pdl(L.PDL_PLANNER):
+        _multi_stage_rounds(ks, taus, n_max, m0, seeds, max_iter, tol, stage0, schedule, st, live,
+                            run, D, dt, dev)
+    # final labels = running argmin over every accumulated centre; drop empty
+    # centres and sort members -- one launch each for every head
+    fin = [h for h in range(H) if results[h] is None]
+    if fin:
+        b = run.batch
+        sub = L.to_device_struct(np.ascontiguousarray(b.desc[fin]))
+        newk = torch.empty(len(fin), dtype=I32, device=dev)
+        L.call("ac_drop_empty", sub.data_ptr(), len(fin), D, b.max_n, b.max_k, newk.data_ptr(),
+               L.stream_ptr())
+        kk = newk.cpu().numpy()
+        for j, p in enumerate(fin):
+            b.desc[p]["k"] = int(kk[j])
+            b.ks[p] = int(kk[j])
+        b.dev = L.to_device_struct(b.desc)
+        sub = L.to_device_struct(np.ascontiguousarray(b.desc[fin]))
+        L.call("ac_sort_by_label", sub.data_ptr(), len(fin), b.max_n, b.max_k, L.stream_ptr())
+        for h in fin:
+            s = st[h]
+            m = b.model(h)
+            m.flag_full = s["flag"]
+            m.stage_count = s["rnd"]
+            m.stage_mse = s["mse"]
+            m.tau = float(taus[h])
+            m.host_iters = s["iters"]
+            results[h] = m
+    return results  # type: ignore[return-value]
+
+
+def _multi_stage_rounds(ks, taus, n_max, m0, seeds, max_iter, tol, stage0, schedule, st, live,
+                        run, D, dt, dev):
+    """The round loop of multi_stage_batch (mutates st / live)."""
     while live:
         todo = []
         for h in live:
@@ -675,32 +709,6 @@ def multi_stage_batch(ks: list[torch.Tensor], taus: list[float], n_max: int, m0:
             if st[h]["nc"] >= n_max:
                 st[h]["flag"] = True
                 live.remove(h)
-    # final labels = running argmin over every accumulated centre; drop empty
-    # centres and sort members -- one launch each for every head
-    fin = [h for h in range(H) if results[h] is None]
-    if fin:
-        b = run.batch
-        sub = L.to_device_struct(np.ascontiguousarray(b.desc[fin]))
-        newk = torch.empty(len(fin), dtype=I32, device=dev)
-        L.call("ac_drop_empty", sub.data_ptr(), len(fin), D, b.max_n, b.max_k, newk.data_ptr(),
-               L.stream_ptr())
-        kk = newk.cpu().numpy()
-        for j, p in enumerate(fin):
-            b.desc[p]["k"] = int(kk[j])
-            b.ks[p] = int(kk[j])
-        b.dev = L.to_device_struct(b.desc)
-        sub = L.to_device_struct(np.ascontiguousarray(b.desc[fin]))
-        L.call("ac_sort_by_label", sub.data_ptr(), len(fin), b.max_n, b.max_k, L.stream_ptr())
-        for h in fin:
-            s = st[h]
-            m = b.model(h)
-            m.flag_full = s["flag"]
-            m.stage_count = s["rnd"]
-            m.stage_mse = s["mse"]
-            m.tau = float(taus[h])
-            m.host_iters = s["iters"]
-            results[h] = m
-    return results  # type: ignore[return-value]
 
 
 # ---------------------------------------------------------------------------
