@@ -224,3 +224,24 @@ def test_lloyd_with_chunked_assign_matches_oracle(gpu, oracle):
     assert np.array_equal(a.assignments, b.assignments)
     assert np.array_equal(a.centers, b.centers)
     assert a.n_iter == b.n_iter
+
+
+@pytest.mark.parametrize("dtype,d", [("f32", 64), ("bf16", 128)])
+def test_pdl_launches_match_plain_launches(gpu, dtype, d):
+    """Programmatic dependent launches of the Lloyd-chain kernels (ac_set_pdl)
+    give the same k-means as plain stream-ordered launches, bit for bit."""
+    from paper_2604_18348_b200 import _lib as L
+    from paper_2604_18348_b200 import engine as E
+    g = torch.Generator().manual_seed(5 + d)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    xs = [(torch.randn(9000 + 501 * h, d, generator=g) * (1 + h)).to(tdt).cuda() for h in range(2)]
+    runs = []
+    for on in (0, 1):
+        with L.pdl(on):
+            ms = E.kmeans_batch(xs, [65, 40], [3, 4], 25, 1e-4)
+        torch.cuda.synchronize()
+        runs.append([(m.centers.clone(), m.labels.clone(), m.n_iter()) for m in ms])
+    for (c0, l0, n0), (c1, l1, n1) in zip(*runs):
+        assert n0 == n1
+        assert torch.equal(l0, l1)
+        assert torch.equal(c0, c1)
