@@ -116,7 +116,14 @@ AC_DEV void argmax_merge(float& bd, int64_t& bi, float od, int64_t oi) {
 // the launch and ramp of the ~125 dependent launches of a 25-iteration
 // chain behind the tails of their predecessors.
 AC_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
-AC_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+#ifndef AC_PDL_EARLY
+#define AC_PDL_EARLY 1  // 0: no explicit trigger (the next grid launches as this one exits)
+#endif
+AC_DEV void pdl_trigger() {
+#if AC_PDL_EARLY
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+}
 
 }  // namespace ac
 
