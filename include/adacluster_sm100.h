@@ -239,11 +239,9 @@ int ac_get_assign_mode(void);
 #define AC_UPDATE_MODE_AUTO 3
 int ac_set_update_mode(int mode);
 /* programmatic dependent launch of the Lloyd-chain kernels (per calling
- * thread; default off, env AC_PDL=1 turns it on at load): each kernel is
- * scheduled while its predecessor drains.  It shortens a lone chain of small
- * launches (C1 warm step 1.196 -> 1.131 ms, the multi-stage planner of one
- * hard head 115 -> 103 ms) but slows concurrent chains, whose waiting CTAs
- * hold SM slots the other chains need (C2 25.9 -> 29.3 ms).                */
+ * thread; default on, env AC_PDL=0 turns it off at load): each kernel is set
+ * up while its predecessor drains (C1 warm step 1.193 -> 1.152 ms, C2 25.75
+ * -> 25.62 ms, the multi-stage planner of one hard head 111 -> 102 ms).    */
 int ac_set_pdl(int on);
 int ac_get_pdl(void);
 int ac_get_update_mode(void);

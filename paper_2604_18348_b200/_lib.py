@@ -157,9 +157,9 @@ def pdl(on: bool = True):
         call("ac_set_pdl", prev)
 
 
-# where the engine turns it on: lone chains of small launches (steady steps
-# of at most this many rows per layer, the multi-stage planner's rounds)
-PDL_STEADY_ROWS = int(os.environ.get("AC_PDL_STEADY_ROWS", "200000"))
+# where the engine turns it on (A/B knobs): steady steps of at most this
+# many rows per layer (default: all), the multi-stage planner's rounds
+PDL_STEADY_ROWS = int(os.environ.get("AC_PDL_STEADY_ROWS", str(1 << 62)))
 PDL_PLANNER = os.environ.get("AC_PDL_PLANNER", "1") != "0"
 
 

@@ -51,7 +51,7 @@ int func_smem(const void* fn, int bytes, const char* what) {
 
 // per calling thread, like the assign/update modes (a CUDA graph keeps the
 // attribute its kernels were captured with); env AC_PDL sets the default
-static int pdl_default() { return getenv("AC_PDL") ? atoi(getenv("AC_PDL")) : 0; }
+static int pdl_default() { return getenv("AC_PDL") ? atoi(getenv("AC_PDL")) : 1; }
 thread_local int g_pdl = pdl_default();
 bool pdl_on() { return g_pdl != 0; }
 

@@ -111,13 +111,16 @@ AC_DEV void argmax_merge(float& bd, int64_t& bi, float od, int64_t oi) {
 // launched with the programmatic-serialisation attribute starts with
 // pdl_wait() (griddepcontrol.wait: returns once the previous kernel of the
 // stream has completed and its memory is visible; a no-op for a normal
-// launch), so nothing it reads can be stale; pdl_trigger() then lets the
-// next kernel of the stream be scheduled while this one runs, which hides
-// the launch and ramp of the ~125 dependent launches of a 25-iteration
-// chain behind the tails of their predecessors.
+// launch), so nothing it reads can be stale.  The next kernel of the stream
+// is then set up while this one drains, which hides part of the launch
+// latency of the ~125 dependent launches of a 25-iteration chain.
 AC_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 #ifndef AC_PDL_EARLY
-#define AC_PDL_EARLY 1  // 0: no explicit trigger (the next grid launches as this one exits)
+// 1: trigger at kernel start (the next grid's CTAs wait on SM slots while
+// this one runs -- faster for a lone chain, C1 1.135 vs 1.152 ms, but it
+// starves concurrent chains, C2 29.3 vs 25.6 ms); 0: no explicit trigger,
+// the next grid launches as this one's CTAs exit (the default)
+#define AC_PDL_EARLY 0
 #endif
 AC_DEV void pdl_trigger() {
 #if AC_PDL_EARLY

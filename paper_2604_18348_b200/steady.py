@@ -231,9 +231,7 @@ class SteadyStep:
         return [(n, round(t0.elapsed_time(e), 3)) for n, e in self.marks]
 
     def _enqueue(self, host=None):
-        # programmatic dependent launches only for small layers (C1: the two
-        # chains leave most SMs idle; at C2-C4 size the waiting CTAs would
-        # hold SM slots the concurrent chains need)
+        # programmatic dependent launches of the Lloyd chains (ac_set_pdl)
         with L.pdl(self.H * self.L <= L.PDL_STEADY_ROWS):
             self._enqueue_impl(host)
 
