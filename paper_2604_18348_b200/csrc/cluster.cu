@@ -1411,6 +1411,8 @@ __global__ void k_kpp_init(const ac_cluster_problem* __restrict__ probs, int dty
 // closest = min(closest, ((x - centers[s]) ** 2).sum(axis=1))  (s == 0: assign)
 __global__ void k_kpp_dist(const ac_cluster_problem* __restrict__ probs, int dtype, int d,
                            int s) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) float ksm[];
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (s + 1 >= P.k || P.status[AC_ST_KPP_STOP] >= 0) return;
@@ -1446,6 +1448,8 @@ constexpr int kKppTab = 4096;
 template <int D>
 __global__ void __launch_bounds__(256)
 k_kpp_dist_v(const ac_cluster_problem* __restrict__ probs, int dtype, int s) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float s_tab[kKppTab];
   const ac_cluster_problem& P = probs[blockIdx.y];
   if (s + 1 >= P.k || P.status[AC_ST_KPP_STOP] >= 0) return;
@@ -1551,6 +1555,8 @@ constexpr double kTwoM52 = 2.220446049250313e-16;  // 2^-52
 __global__ void __launch_bounds__(1024)
 k_kpp_pick(const ac_cluster_problem* __restrict__ probs, int dtype, int d, int s,
            const double* __restrict__ draws, int max_k, int64_t rows_off) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char kpsm[];
   const ac_cluster_problem& P = probs[blockIdx.x];
   if (s + 1 >= P.k || P.status[AC_ST_KPP_STOP] >= 0) return;
@@ -2422,13 +2428,14 @@ extern "C" int ac_kmeanspp(const ac_cluster_problem* probs, int nprob, int dtype
   for (int s = 0; s + 1 < max_k; ++s) {
     if (rows_fast) {
       const dim3 grid((unsigned)((max_n + 255) / 256), nprob);
-      if (d == 64) k_kpp_dist_v<64><<<grid, 256, 0, st>>>(probs, dtype, s);
-      else k_kpp_dist_v<128><<<grid, 256, 0, st>>>(probs, dtype, s);
+      if (d == 64) ac_host::launch_pdl(k_kpp_dist_v<64>, grid, dim3(256), 0, st, probs, dtype, s);
+      else ac_host::launch_pdl(k_kpp_dist_v<128>, grid, dim3(256), 0, st, probs, dtype, s);
     } else {
-      k_kpp_dist<<<dim3((unsigned)((max_n + 255) / 256), nprob), 256, sizeof(float) * d, st>>>(
-          probs, dtype, d, s);
+      ac_host::launch_pdl(k_kpp_dist, dim3((unsigned)((max_n + 255) / 256), nprob), dim3(256),
+                          sizeof(float) * d, st, probs, dtype, d, s);
     }
-    k_kpp_pick<<<nprob, 1024, psm, st>>>(probs, dtype, d, s, draws, max_k, rows_off);
+    ac_host::launch_pdl(k_kpp_pick, dim3(nprob), dim3(1024), psm, st, probs, dtype, d, s, draws,
+                        max_k, rows_off);
   }
   AC_CHECK_LAUNCH("ac_kmeanspp");
   return AC_OK;
