@@ -230,8 +230,8 @@ int ac_get_assign_mode(void);
  * enclosure-tested sums streamed over contiguous row ranges (every SM
  * busy, no walk of a whole cluster by one warp; needs the csum/cabs/clsb
  * workspaces and k <= 1024, else as mode 0), 3 = AUTO (the default): mode 2
- * for batches with fewer than 512 centres in total (multi-stage planner
- * rounds), mode 1 otherwise.  All are bit-identical to np.add.reduceat in
+ * for batches with fewer than 512 centres in total and >= 128 rows per
+ * centre (multi-stage planner rounds), mode 1 otherwise.  All are bit-identical to np.add.reduceat in
  * member order.  Env AC_UPDATE_MODE overrides the default at load.        */
 #define AC_UPDATE_MODE_SPLIT 0
 #define AC_UPDATE_MODE_MEMBER 1

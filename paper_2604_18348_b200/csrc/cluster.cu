@@ -2273,18 +2273,22 @@ static bool usum_ok(const ac_cluster_problem* host_probs, int nprob, int dtype, 
 
 // Update kernel of a Lloyd run.  The member-order kernel runs one warp per
 // centre on ceil(k / kUpdWarps) CTAs per problem: in a batch with few centres
-// in total (the multi-stage planner's rounds: one to a few heads, m_t = 8..100
-// centres) most SMs idle while single warps walk clusters of thousands of
-// members, so such batches take the streamed sums, which spread the rows
-// over every SM (one "mixed" C3 head's planner: 133 ms of member-order
-// updates over 925 launches).  Larger batches keep the default.
+// in total and long clusters (the multi-stage planner's rounds: one to a few
+// heads, m_t = 8..100 centres over thousands of rows) most SMs idle while
+// single warps walk clusters of thousands of members, so such batches take
+// the streamed sums, which spread the rows over every SM (one "mixed" C3
+// head's planner: 133 ms of member-order updates over 925 launches).  Short
+// clusters (C1: 4,096 rows over 65 centres, warm step 1.07 vs 1.15 ms) and
+// larger batches keep the member-order kernel.
 static int update_mode_for(const ac_cluster_problem* host_probs, int nprob, int dtype, int d,
-                           int max_k) {
+                           int64_t max_n, int max_k) {
   static const int small = getenv("AC_USM_SMALL") ? atoi(getenv("AC_USM_SMALL")) : 512;
+  static const int per_centre = getenv("AC_USM_ROWS") ? atoi(getenv("AC_USM_ROWS")) : 128;
   const int mode = g_update_mode;
   if (mode == AC_UPDATE_MODE_MEMBER) return mode;
   if (mode == AC_UPDATE_MODE_AUTO) {
-    if ((int64_t)nprob * max_k < small && max_k <= kUsmMaxK && usum_ws(host_probs, nprob, d))
+    if ((int64_t)nprob * max_k < small && max_n >= (int64_t)per_centre * max_k &&
+        max_k <= kUsmMaxK && usum_ws(host_probs, nprob, d))
       return AC_UPDATE_MODE_STREAM;
     return AC_UPDATE_MODE_MEMBER;
   }
@@ -2346,7 +2350,7 @@ static int lloyd_impl(const ac_cluster_problem* probs, int nprob, int dtype, int
   const int lo_flag = (!inertia && g_assign_mode != AC_ASSIGN_MODE_EXACT &&
                        ac_host::assign_tc_eligible(host_probs, nprob, dtype, d, 0, order))
                           ? AC_ASSIGN_LABELS_ONLY : 0;
-  const int umode = update_mode_for(host_probs, nprob, dtype, d, max_k);
+  const int umode = update_mode_for(host_probs, nprob, dtype, d, max_n, max_k);
   int rc = prepare_impl(probs, nprob, dtype, d, max_n, max_k, (lflags & AC_LLOYD_PREPARED) != 0,
                         stream);
   if (rc) return rc;
