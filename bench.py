@@ -428,6 +428,50 @@ def dense_baselines(trip, tdt, with_flashinfer=True) -> dict:
     return res
 
 
+def dense_e2e_ms(host_trip, tdt, chunks: int = 4, reps: int = 3) -> float:
+    """The fastest dense kernel (cuDNN SDPA) end to end from the same pinned
+    host Q/K/V into a pinned host result: head chunks pipelined over three
+    streams (H2D of chunk c+1 and D2H of chunk c-1 overlap the attention of
+    chunk c), so the dense baseline gets the same copy overlap as ours."""
+    import torch
+    import torch.nn.functional as F
+    hq, hk, hv = host_trip
+    H = hq.shape[0]
+    out_h = torch.empty(hq.shape, dtype=tdt).pin_memory()
+    dq, dk, dv = (torch.empty(hq.shape, dtype=tdt, device="cuda") for _ in range(3))
+    do = torch.empty(hq.shape, dtype=tdt, device="cuda")
+    s_in, s_c, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    bounds = [(H * c) // chunks for c in range(chunks + 1)]
+
+    def run():
+        main = torch.cuda.current_stream()
+        s_in.wait_stream(main)
+        s_c.wait_stream(main)
+        s_out.wait_stream(main)
+        for c in range(chunks):
+            h0, h1 = bounds[c], bounds[c + 1]
+            if h1 <= h0:
+                continue
+            with torch.cuda.stream(s_in):
+                for src, dst in ((hq, dq), (hk, dk), (hv, dv)):
+                    dst[h0:h1].copy_(src[h0:h1], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_in)
+            s_c.wait_event(ev_in)
+            with torch.cuda.stream(s_c):
+                do[h0:h1] = F.scaled_dot_product_attention(
+                    dq[h0:h1].unsqueeze(0), dk[h0:h1].unsqueeze(0), dv[h0:h1].unsqueeze(0))[0]
+                ev_c = torch.cuda.Event()
+                ev_c.record(s_c)
+            s_out.wait_event(ev_c)
+            with torch.cuda.stream(s_out):
+                out_h[h0:h1].copy_(do[h0:h1], non_blocking=True)
+        main.wait_stream(s_out)
+        main.synchronize()  # result ready on the host, as for LayerSession.step
+
+    return _time_cuda(run, reps)
+
+
 def count_launches(step_fn) -> int:
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -616,6 +660,11 @@ def run_layer(args, cfg, world, rank, local):
     dense = None
     if not args.no_dense and rank == 0 and my:
         dense = dense_baselines(dev_in[0], tdt)
+        if not args.no_e2e and world == 1:
+            try:
+                dense["sdpa_cudnn_e2e_ms"] = dense_e2e_ms(host[0], tdt)
+            except RuntimeError as exc:
+                dense["sdpa_cudnn_e2e_ms"] = f"failed: {exc}"[:200]
 
     # ---- parity block + CPU baseline (rank 0, N = 1) ----
     parity, cpu = None, None
@@ -656,6 +705,9 @@ def run_layer(args, cfg, world, rank, local):
         }
         if dense and dense.get("fastest_ms"):
             line["speedup_vs_fastest_dense"] = dense["fastest_ms"] / ms
+            if e2e and isinstance(dense.get("sdpa_cudnn_e2e_ms"), float):
+                # both from the same pinned host buffers into a host result
+                line["e2e_speedup_vs_dense_e2e"] = dense["sdpa_cudnn_e2e_ms"] / e2e["ms_per_step"]
         if args.breakdown:
             line["cold_phases_ms"] = cold_breakdown
         print(json.dumps(line), flush=True)
