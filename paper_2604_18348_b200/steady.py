@@ -202,8 +202,13 @@ class SteadyStep:
         self.host_graphs = {}
         self.joins = [torch.cuda.Event() for _ in range(2 * nblk)]
         # host path: the attention runs in head chunks, each chunk's output
-        # copied back (D2H stream) while the next chunk computes
-        self.out_chunks = max(1, min(H, int(os.environ.get("AC_STEADY_OUT_CHUNKS", "5"))))
+        # copied back (D2H stream) while the next chunk computes: about 34 MB
+        # of output per chunk, at most 5 (e2e ms for 1/2/3/5 chunks: C1
+        # 1.18/1.44/1.46/1.44, C3 9.93/8.61/8.42/8.62, C2 -/30.8/29.9/29.5,
+        # C4 -/81.3/80.2/80.5); AC_STEADY_OUT_CHUNKS overrides
+        out_bytes = H * Ln * D * self.out.element_size()
+        chunks = min(5, max(1, -(-out_bytes // (34 << 20))))
+        self.out_chunks = max(1, min(H, int(os.environ.get("AC_STEADY_OUT_CHUNKS", chunks))))
         self.d2h = torch.cuda.Stream()
         self.vstream = torch.cuda.Stream()
         self.v_in = [torch.cuda.Event() for _ in range(self.out_chunks)]
