@@ -66,6 +66,10 @@ class Workspace:
 # measured the same or faster (C3 5.43-5.47 vs 5.44-5.49 ms, C4 71.7-71.9
 # vs 72.2-72.5 ms same box)
 _ORDER_ITEMS = os.environ.get("AC_ITEM_ORDER", "0") != "0"
+# host path H2D order: every block's Q, then every block's K (default), or
+# interleaved Q0 K0 Q1 K1 (AC_H2D_QFIRST=0); e2e C2 29.52 -> 28.04 ms, C4
+# 79.4 -> 77.5, C3 8.39 -> 8.34 same box
+_H2D_QFIRST = os.environ.get("AC_H2D_QFIRST", "1") != "0"
 
 
 class SteadyStep:
@@ -250,7 +254,8 @@ class SteadyStep:
         latency-bound launches that leaves most SMs idle.
 
         ``host = (hQ, hK, hV, hout)`` (pinned) puts the PCIe copies into the
-        graph: Q first (the query chain is the longest), then K, then V,
+        graph: every block's Q first (the query chains are the longest), then
+        K, then V,
         each overlapping the clustering already running; the result is copied
         back at the end."""
         H, Ln, D = self.H, self.L, self.D
@@ -262,18 +267,24 @@ class SteadyStep:
         self.ev[0].record()
         self.fork.record(main)
         # host path: per-block H2D copies on their own stream in the order the
-        # chains need them (Q0 K0 Q1 K1 ... V), so block 0's clustering starts
-        # after 1/(2*nblk) of the input has arrived instead of all of Q
+        # chains need them (Q0 Q1 .. K0 K1 .. V: the query chains are the
+        # long ones), so block 0's query clustering starts after 1/(3*nblk)
+        # of the input has arrived
         if host is not None:
             self.h2d.wait_event(self.fork)
+            # AC_H2D_QFIRST=1: every block's Q before any K (the query chains
+            # are the long ones), else interleaved Q0 K0 Q1 K1
+            order = ([(0, i) for i in range(len(blocks))] + [(1, i) for i in range(len(blocks))]
+                     if _H2D_QFIRST else [(t, i) for i in range(len(blocks)) for t in (0, 1)])
+            with torch.cuda.stream(self.h2d):
+                for t, i in order:
+                    h0, h1 = blocks[i]
+                    dst = self.Q if t == 0 else self.K
+                    dst[h0:h1].copy_(host[t][h0:h1], non_blocking=True)
+                    (self.q_in if t == 0 else self.k_in)[i].record(self.h2d)
         for i, (h0, h1) in enumerate(blocks):
             qs, ks = self.streams[2 * i + 1], self.streams[2 * i]
             if host is not None:
-                with torch.cuda.stream(self.h2d):
-                    self.Q[h0:h1].copy_(host[0][h0:h1], non_blocking=True)
-                    self.q_in[i].record(self.h2d)
-                    self.K[h0:h1].copy_(host[1][h0:h1], non_blocking=True)
-                    self.k_in[i].record(self.h2d)
                 qs.wait_event(self.q_in[i])
                 ks.wait_event(self.k_in[i])
             else:
